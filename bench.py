@@ -1,0 +1,350 @@
+"""Benchmark: exact k-NN QPS, 1M x 128 fp32, k=10 (BASELINE.json metric, cfg2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
+
+One step = one search of all nq=10k queries against the whole database
+(1M x 128 fp32, 3xTF32, L2, k=10), inputs already resident in HBM.  For N>1
+(torchrun, one rank per GPU) the database rows are sharded over the ranks
+(strong scaling: fixed database, fixed nq), every rank searches its shard and
+the per-shard top-k lists are all-gathered over NCCL and merged.
+
+Printed (rank 0, one JSON line): value (QPS), e2e (same metric through the
+public API with host buffers: H2D of the queries and D2H of the results
+inside the timed region), roofline of the fused GEMM+top-k kernel (CUDA
+events on its launch stream, during the timed region), the CPU baseline (the
+oracle port of the reference, bounded sample, N=1 only), clocks sampled with
+nvidia-smi during the timed region, and the kernel launch count.
+
+``--impl reference`` times the reference's CPU algorithm (oracle port of
+annkit flat_search_blas, numpy/OpenBLAS on all host cores) on a bounded query
+sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+CONFIGS = {
+    1: dict(name="cfg1: IndexFlatL2 nb=100k d=128 nq=1k k=10 fp32 (3xTF32)", nb=100_000, d=128, nq=1_000, k=10,
+            metric="l2", storage="fp32"),
+    2: dict(name="cfg2: IndexFlatL2 nb=1M d=128 nq=10k k=10 fp32 (3xTF32)", nb=1_000_000, d=128, nq=10_000, k=10,
+            metric="l2", storage="fp32"),
+    3: dict(name="cfg3: IndexFlatL2 nb=1M d=128 nq=10k k=1024 fp32 (3xTF32)", nb=1_000_000, d=128, nq=10_000,
+            k=1024, metric="l2", storage="fp32"),
+    4: dict(name="cfg4: IndexFlatIP nb=10M d=768 nq=10k k=100 fp16", nb=10_000_000, d=768, nq=10_000, k=100,
+            metric="ip", storage="fp16"),
+    5: dict(name="cfg5: IndexFlatL2 nb=100M d=96 nq=10k k=10 bf16", nb=100_000_000, d=96, nq=10_000, k=10,
+            metric="l2", storage="bf16"),
+}
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+L2_BYTES = 126 * 2**20
+
+
+def load_peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def gen_base(cfg, lo=0, hi=None):
+    """Seeded synthetic base rows [lo, hi) (default_rng(0), per-1M chunks beyond 1M)."""
+    nb, d = cfg["nb"], cfg["d"]
+    hi = nb if hi is None else hi
+    if nb <= 1_000_000:
+        return np.random.default_rng(0).standard_normal((nb, d), dtype=np.float32)[lo:hi]
+    out = np.empty((hi - lo, d), np.float32)
+    c0 = lo // 1_000_000
+    for c in range(c0, (hi + 999_999) // 1_000_000):
+        blk = np.random.default_rng([0, c]).standard_normal((1_000_000, d), dtype=np.float32)
+        a, b = max(lo, c * 1_000_000), min(hi, (c + 1) * 1_000_000)
+        out[a - lo:b - lo] = blk[a - c * 1_000_000:b - c * 1_000_000]
+    return out
+
+
+def gen_queries(cfg):
+    return np.random.default_rng(1).standard_normal((cfg["nq"], cfg["d"]), dtype=np.float32)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_oracle_qps(xb, q, k, metric, nq_sample):
+    """Reference algorithm (oracle port of annkit flat_search_blas) on host cores."""
+    from oracle import flat_oracle as O
+    norms = O.add_norms(xb)
+    t0 = time.perf_counter()
+    O.flat_search_blas(xb, q[:nq_sample], k, metric, norms=norms)
+    dt = time.perf_counter() - t0
+    return nq_sample / dt, dt
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        for info in threadpool_info():
+            if info.get("internal_api") in ("openblas", "mkl", "blis"):
+                return int(info.get("num_threads", os.cpu_count()))
+    except Exception:
+        pass
+    return os.cpu_count()
+
+
+def run_reference(args, cfg):
+    """--impl reference: the reference CPU path on a bounded sample per step."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    xb = gen_base(cfg, 0, min(cfg["nb"], 1_000_000))
+    q = gen_queries(cfg)
+    scale = cfg["nb"] / xb.shape[0]  # cost is linear in nb (flat.py:106-118)
+    nq_s = 128
+    for _ in range(args.warmup):
+        cpu_oracle_qps(xb, q, cfg["k"] if cfg["k"] <= xb.shape[0] else xb.shape[0], cfg["metric"], nq_s)
+    times = []
+    for _ in range(args.steps):
+        _, dt = cpu_oracle_qps(xb, q, cfg["k"], cfg["metric"], nq_s)
+        times.append(dt * scale)
+    ms = statistics.median(times) * 1e3
+    qps = nq_s / (ms / 1e3)
+    cores = blas_threads()
+    sample = f"{nq_s} of {cfg['nq']} queries per step x {xb.shape[0]} base rows" + (
+        f", time x{scale:g} for nb={cfg['nb']}" if scale != 1 else "")
+    line = {
+        "impl": "reference", "metric": "exact k-NN QPS (1M x 128, k=10)", "value": qps, "unit": "queries/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg["name"], "nb": cfg["nb"], "d": cfg["d"], "nq": cfg["nq"], "k": cfg["k"],
+                   "parallelism": "cpu"},
+        "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    from paper_2401_08281_b200 import METRIC_IP, METRIC_L2, FlatIndex, ShardedFlatIndex
+    metric = METRIC_L2 if cfg["metric"] == "l2" else METRIC_IP
+    nb, d, nq, k = cfg["nb"], cfg["d"], cfg["nq"], cfg["k"]
+
+    # ---- build (untimed)
+    if world == 1:
+        index = FlatIndex(d, metric, storage=cfg["storage"], device=local)
+        step = 2_000_000
+        for lo in range(0, nb, step):
+            xb_part = gen_base(cfg, lo, min(nb, lo + step))
+            index.add(torch.from_numpy(xb_part).cuda())
+        local_index = index
+    else:
+        from paper_2401_08281_b200.sharded import shard_range
+        index = ShardedFlatIndex(d, metric, storage=cfg["storage"], device=local)
+        lo, hi = shard_range(nb, rank, world)
+        xb_part = gen_base(cfg, lo, hi)
+        index.add_local_shard(torch.from_numpy(xb_part).cuda(), lo, nb)
+        local_index = index.local
+    q_np = gen_queries(cfg)
+    q_dev = torch.from_numpy(q_np).cuda()
+    q_host = torch.from_numpy(q_np).pin_memory()
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def maxr(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        index.search(q_dev, k)
+    torch.cuda.synchronize()
+
+    # ---- timed region: device-resident inputs
+    local_index.set_profiling(True)
+    local_index.kernel_times()  # reset accumulators
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            res = index.search(q_dev, k)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms_local = ev0.elapsed_time(ev1) / args.steps
+    ms = maxr(ms_local)
+    (t_prep, t_fused, t_merge), launches = local_index.kernel_times()
+    local_index.set_profiling(False)
+    plan = local_index.last_plan()
+    value = nq / (ms / 1e3)
+
+    # ---- e2e through the public API with host buffers (H2D + D2H inside)
+    for _ in range(max(1, args.warmup // 2)):
+        index.search(q_host, k)
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r = index.search(q_host, k)  # returns host numpy arrays
+    torch.cuda.synchronize()
+    e2e_ms = maxr((time.perf_counter() - t0) * 1e3 / args.steps)
+    assert isinstance(r.ids, np.ndarray)
+
+    peaks, peaks_kind = load_peaks()
+    # algorithmic work of one fused launch (local shard): 2*nq*nb_local*d flops
+    nb_local = local_index.ntotal
+    flops = 2.0 * nq * nb_local * d
+    passes = 3 if cfg["storage"] == "fp32" else 1
+    tc_peak = peaks["bf16_tflops"] / (2.0 if cfg["storage"] == "fp32" else 1.0) / passes
+    achieved = flops / (t_fused / 1e3) / 1e12
+    elem = 4 if cfg["storage"] == "fp32" else 2
+    alg_bytes = nb_local * d * elem * (2 if cfg["storage"] == "fp32" else 1) + nb_local * 4 + nq * d * elem * 2 \
+        + nq * k * 8
+    line = {
+        "metric": "exact k-NN QPS (1M x 128, k=10)" if args.config == 2 else f"exact k-NN QPS ({cfg['name']})",
+        "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32 (3xTF32 tensor-core split)" if cfg["storage"] == "fp32" else cfg["storage"],
+        "data": "synthetic (numpy default_rng(0/1) standard normal, SURVEY 8(d))",
+        "config": {"workload": cfg["name"], "nb": nb, "d": d, "nq": nq, "k": k, "metric": cfg["metric"],
+                   "storage": cfg["storage"],
+                   "l2_flush": "inputs larger than L2: base hi+lo %.2f GB vs 126 MB L2" % (
+                       nb_local * d * elem * (2 if cfg["storage"] == "fp32" else 1) / 1e9),
+                   "parallelism": f"database rows sharded over {world} GPU(s), queries replicated, "
+                                  "NCCL all-gather + merge kernel" if world > 1 else "1 GPU",
+                   "plan": plan},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": tc_peak, "unit": "TFLOP/s",
+                     "frac": achieved / tc_peak, "traffic": None,
+                     "kernel": "fused_knn_kernel (tcgen05 GEMM + fused top-k)",
+                     "kernel_ms": t_fused, "prep_ms": t_prep, "merge_ms": t_merge,
+                     "alg_flops_per_launch": flops, "alg_bytes_per_launch": alg_bytes,
+                     "peak_note": f"{peaks_kind} bf16 {peaks['bf16_tflops']} TF/s"
+                                  + (" / 2 (tf32 rate) / 3 (3xTF32 passes)" if cfg["storage"] == "fp32" else "")},
+        "e2e": {"value": nq / (e2e_ms / 1e3), "unit": "queries/s", "h2d_bytes_per_step": int(q_np.nbytes),
+                "d2h_bytes_per_step": int(nq * k * (4 + 8)), "ms_per_step": e2e_ms},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if world > 1:
+        line["gpu_launches_note"] = "per rank; plus NCCL all-gather kernels"
+    # ---- CPU baseline (rank 0, N=1 only): oracle port on a bounded sample
+    if world == 1 and not args.no_cpu_baseline:
+        xb_cpu = gen_base(cfg, 0, min(nb, 1_000_000))
+        scale = nb / xb_cpu.shape[0]
+        nq_s = 256
+        qps, dt = cpu_oracle_qps(xb_cpu, q_np, k, cfg["metric"], nq_s)
+        line["cpu_baseline"] = {"value": qps / scale, "unit": "queries/s", "cores": blas_threads(), "kind": "port",
+                                "sample": f"{nq_s} of {nq} queries x {xb_cpu.shape[0]} base rows ({dt:.1f} s)"
+                                          + (f", scaled x1/{scale:g}" if scale != 1 else "")}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

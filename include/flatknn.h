@@ -1,0 +1,124 @@
+/*
+ * flatknn.h -- C ABI of the B200-native exact flat k-NN engine (libflatknn.so).
+ *
+ * Drop-in boundary for the reference's exhaustive-search hot path
+ * (arxiv/paper_2401_08281 reference, package `annkit`, /root/reference/pkg):
+ *
+ *   reference interface                                   replaced by
+ *   ----------------------------------------------------  -------------------------
+ *   FlatIndex.__init__(d, metric)      flat.py:21-26      fk_create
+ *   FlatIndex._add(x, ids)             flat.py:28-32      fk_add
+ *     (norms einsum at add             flat.py:31)
+ *   FlatIndex._search(q, k)            flat.py:58-62      fk_search
+ *     flat_search_blas                 flat.py:94-118
+ *     topk_rows / _monotone_key        core.py:193-236
+ *     _finish (position -> id)         flat.py:68-73
+ *   FlatIndex.ntotal                   core.py:118,143    fk_ntotal
+ *   (Faiss-style reset; none in ref)   SURVEY 8(b)        fk_reset
+ *   FlatIndex.reconstruct_batch        flat.py:43-44      fk_reconstruct
+ *   FlatIndex.remove_ids               flat.py:46-56      fk_remove_ids
+ *   _kernels function table errors     _kernels/__init__.py:37-41 -> fk_last_error
+ *   (none: SPEC.md:115 non-goal)       SURVEY 8(e)        fk_merge_shards
+ *
+ * Conventions: plain pointers and sizes only.  Every entry point returns 0 on
+ * success or a negative FK_E* code; fk_last_error() then returns a message
+ * (thread-local).  `stream` is a cudaStream_t (NULL = legacy default stream).
+ * `on_device` != 0 means every data pointer of that call is CUDA device memory
+ * on the index's device; otherwise they are host pointers (pinned memory gives
+ * asynchronous copies; pageable memory works but copies synchronously).
+ * Results are written in the reference's order: best first, ties broken by the
+ * smaller storage position, k > ntotal padded with id -1 and +inf (L2) / -inf
+ * (IP).
+ */
+#ifndef FLATKNN_H_
+#define FLATKNN_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fk_index fk_index;
+
+/* metric codes: same values as annkit _pykernels.M_IP / M_L2 (_pykernels.py:14-15) */
+#define FK_METRIC_IP 0
+#define FK_METRIC_L2 1
+
+/* storage / input dtypes */
+#define FK_F32 0  /* storage: fp32, searched with a 3xTF32 split (fp32-faithful) */
+#define FK_F16 1  /* storage: fp16 (RNE from f32), tensor-core kind::f16      */
+#define FK_BF16 2 /* storage: bf16 (RNE from f32), tensor-core kind::f16      */
+
+/* error codes */
+#define FK_OK 0
+#define FK_E_INVALID -1     /* bad argument (ValueError in the Python mirror)  */
+#define FK_E_CUDA -2        /* CUDA runtime / driver failure                  */
+#define FK_E_NOMEM -3       /* device allocation failed                       */
+#define FK_E_UNSUPPORTED -4 /* valid but not supported (NotImplementedError)  */
+#define FK_E_NOTFOUND -5    /* unknown id (KeyError, flat.py:40-41)            */
+
+/* Create an empty index on CUDA device `device` (flat.py:21-26). */
+int fk_create(int device, int d, int metric, int storage, fk_index** out);
+
+/* Append n vectors (row-major n x d of `dtype`) with int64 ids (flat.py:28-32;
+ * ids == NULL -> sequential ntotal..ntotal+n-1, core.py:128-131).  Ids are
+ * validated (>= 0) by the caller, as core.py:139-141 does.  Base norms are
+ * computed on device from the stored (rounded) values. */
+int fk_add(fk_index* h, const void* x, int64_t n, int dtype, const int64_t* ids, int on_device,
+           void* stream);
+
+/* Exact top-k for nq queries (row-major nq x d of `dtype`).
+ * D: nq x k float32 distances (L2: squared, clamped at 0; IP: inner product).
+ * I: nq x k int64 ids (-1 for padding).
+ * P: optional (may be NULL) nq x k int64 storage positions (-1 for padding),
+ *    needed to order ties across shards (fk_merge_shards). */
+int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D, int64_t* I, int64_t* P,
+              int on_device, void* stream);
+
+/* Merge per-shard results into the single-index answer.  Inputs are
+ * nshard x nq x k arrays (shard-major) of distances, GLOBAL storage positions
+ * and ids, each shard's rows already best-first.  Output ordered by
+ * (distance, global position) exactly like a single unsharded index.  All
+ * pointers are device pointers on the current device. */
+int fk_merge_shards(int metric, int nshard, int64_t nq, int k, const float* D_in, const int64_t* P_in,
+                    const int64_t* I_in, float* D_out, int64_t* I_out, void* stream);
+
+/* Copy the stored vectors of the given storage positions back as float32
+ * (flat.py:43-44 reconstruct_batch; the Python mirror maps ids->positions). */
+int fk_reconstruct(fk_index* h, const int64_t* positions, int64_t n, float* out, int on_device, void* stream);
+
+/* Remove every stored vector whose id is in ids[0..n) (flat.py:46-56),
+ * compacting storage in place and preserving order.  *removed = count. */
+int fk_remove_ids(fk_index* h, const int64_t* ids, int64_t n, int on_device, int64_t* removed, void* stream);
+
+/* Drop all vectors, keep the device allocation (Faiss Index::reset). */
+int fk_reset(fk_index* h);
+
+int64_t fk_ntotal(const fk_index* h);
+int fk_dim(const fk_index* h);
+
+/* Copy the ids table (ntotal int64) to host memory. */
+int fk_get_ids(fk_index* h, int64_t* out_host);
+
+void fk_destroy(fk_index* h);
+
+const char* fk_last_error(void);
+
+/* Instrumentation: when enabled, fk_search records CUDA events around each of
+ * its kernels on the launch stream (no host synchronisation).  fk_kernel_times
+ * waits for them and returns the mean durations (ms) per search since its
+ * previous call: [0] query prep, [1] fused GEMM+top-k, [2] merge; *nlaunch =
+ * total kernel launches of those searches.  Then it resets the accumulators. */
+int fk_set_profiling(fk_index* h, int on);
+int fk_kernel_times(fk_index* h, float* ms3, int* nlaunch);
+
+/* Tuning / introspection of the last search plan: grid size, number of
+ * N-chunks (split-N), tile sizes, pipeline stages. */
+int fk_last_plan(fk_index* h, int* out8);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FLATKNN_H_ */

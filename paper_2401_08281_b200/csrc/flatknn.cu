@@ -1,0 +1,686 @@
+// libflatknn.so -- C ABI (include/flatknn.h) over the sm_100a flat k-NN kernels.
+//
+// Host side of the drop-in for the reference FlatIndex hot path
+// (/root/reference/pkg/src/annkit/flat.py:14-118, core.py:107-236).
+// Owns device storage (operand layout + norms + ids), plans the persistent
+// fused GEMM+top-k launch (split-N work units ordered for L2 reuse), encodes
+// the TMA tensor maps and runs prep -> fused -> merge on the caller's stream.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cstdarg>
+#include <cstdlib>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/flatknn.h"
+#include "flatknn_kernels.cuh"
+
+using namespace fk;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int set_err(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(expr)                                                                                         \
+  do {                                                                                                   \
+    cudaError_t e_ = (expr);                                                                             \
+    if (e_ != cudaSuccess)                                                                               \
+      return set_err(e_ == cudaErrorMemoryAllocation ? FK_E_NOMEM : FK_E_CUDA, "%s failed: %s (%s:%d)", \
+                     #expr, cudaGetErrorString(e_), __FILE__, __LINE__);                                 \
+  } while (0)
+
+#define CKL()                                                                                       \
+  do {                                                                                              \
+    cudaError_t e_ = cudaGetLastError();                                                            \
+    if (e_ != cudaSuccess)                                                                          \
+      return set_err(FK_E_CUDA, "kernel launch failed: %s (%s:%d)", cudaGetErrorString(e_), __FILE__, \
+                     __LINE__);                                                                     \
+  } while (0)
+
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                      CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                      CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled_t get_encode() {
+  static PFN_encodeTiled_t fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled_t>(p);
+  });
+  return fn;
+}
+
+// 2-D row-major [rows][cols] tensor, box = 128 bytes of K x 128 rows, SW128.
+int make_map(CUtensorMap* m, const void* base, int elem_bytes, uint64_t cols, uint64_t rows) {
+  PFN_encodeTiled_t enc = get_encode();
+  if (!enc) return set_err(FK_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const CUtensorMapDataType dt = elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT16;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * (cuuint64_t)elem_bytes};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / elem_bytes), 128};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(FK_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return FK_OK;
+}
+
+constexpr int SMEM_LIMIT = 232448;  // sm_100 max dynamic smem per block (227 KB)
+constexpr int SMEM_RESERVE = 1024 /*align*/ + 256 /*barriers + tmem slot*/;
+
+int elem_bytes_of(int storage) { return storage == FK_F32 ? 4 : 2; }
+int chunk_elems_of(int storage) { return storage == FK_F32 ? 32 : 64; }
+int split_of(int storage) { return storage == FK_F32 ? 2 : 1; }
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  int ensure(size_t want) {
+    if (want <= bytes) return FK_OK;
+    release();
+    size_t b = std::max<size_t>(want, 256);
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      return set_err(FK_E_NOMEM, "cudaMalloc(%zu) failed: %s", b, cudaGetErrorString(e));
+    }
+    bytes = b;
+    return FK_OK;
+  }
+};
+
+}  // namespace
+
+struct fk_index {
+  int device = 0, d = 0, dp = 0, metric = FK_METRIC_L2, storage = FK_F32;
+  int64_t ntotal = 0, cap = 0;
+  void* s0 = nullptr;        // stored operand (hi / f16 / bf16) [cap][dp]
+  void* s1 = nullptr;        // lo part (fp32 mode) [cap][dp]
+  float* norms = nullptr;    // [cap]
+  int64_t* ids = nullptr;    // [cap]
+  DevBuf q_in, q0, q1, qn, pkey, ppos, outD, outI, outP, stage_in, stage_ids;
+  std::mutex mu;
+  int num_sms = 148;
+  int profiling = 0;
+  // profiling: one quad of events per search (prep / fused / merge), read
+  // lazily by fk_kernel_times so the timed loop never synchronises the host
+  std::vector<std::array<cudaEvent_t, 4>> ev_pool;
+  size_t ev_used = 0;
+  int nlaunch = 0;        // launches of the last search
+  long long nlaunch_acc = 0;  // launches since the last fk_kernel_times
+  int plan[8] = {0};
+  float* dbg_ip = nullptr;  // test hook (FK_DEBUG_IP)
+};
+
+namespace {
+
+cudaEvent_t* next_events(fk_index* h) {
+  if (h->ev_used == h->ev_pool.size()) {
+    std::array<cudaEvent_t, 4> q{};
+    for (auto& e : q)
+      if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    h->ev_pool.push_back(q);
+  }
+  return h->ev_pool[h->ev_used++].data();
+}
+
+size_t row_bytes(const fk_index* h) { return (size_t)h->dp * elem_bytes_of(h->storage); }
+
+int grow(fk_index* h, int64_t need, cudaStream_t st) {
+  if (need <= h->cap) return FK_OK;
+  int64_t nc = std::max<int64_t>(need, h->cap * 2);
+  nc = std::max<int64_t>(nc, 1024);
+  nc = (nc + BN - 1) / BN * BN;
+  const size_t rb = row_bytes(h);
+  void *n0 = nullptr, *n1 = nullptr;
+  float* nn = nullptr;
+  int64_t* ni = nullptr;
+  cudaError_t e = cudaMalloc(&n0, nc * rb);
+  if (e == cudaSuccess && h->storage == FK_F32) e = cudaMalloc(&n1, nc * rb);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&nn, nc * sizeof(float));
+  if (e == cudaSuccess) e = cudaMalloc((void**)&ni, nc * sizeof(int64_t));
+  if (e != cudaSuccess) {
+    cudaFree(n0);
+    cudaFree(n1);
+    cudaFree(nn);
+    cudaFree(ni);
+    return set_err(FK_E_NOMEM, "device allocation of %lld rows failed: %s", (long long)nc, cudaGetErrorString(e));
+  }
+  CK(cudaMemsetAsync(nn, 0, nc * sizeof(float), st));
+  if (h->ntotal > 0) {
+    CK(cudaMemcpyAsync(n0, h->s0, h->ntotal * rb, cudaMemcpyDeviceToDevice, st));
+    if (n1) CK(cudaMemcpyAsync(n1, h->s1, h->ntotal * rb, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(nn, h->norms, h->ntotal * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(ni, h->ids, h->ntotal * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  cudaFree(h->s0);
+  cudaFree(h->s1);
+  cudaFree(h->norms);
+  cudaFree(h->ids);
+  h->s0 = n0;
+  h->s1 = n1;
+  h->norms = nn;
+  h->ids = ni;
+  h->cap = nc;
+  return FK_OK;
+}
+
+int launch_prep(int storage, const void* x, int dtype, int64_t n, int d, int dp, void* o0, void* o1, float* norms,
+                int64_t row0, cudaStream_t st) {
+  if (n <= 0) return FK_OK;
+  const int wpb = 8;
+  const unsigned grid = (unsigned)((n + wpb - 1) / wpb);
+  if (storage == FK_F32)
+    prep_rows_kernel<0><<<grid, wpb * 32, 0, st>>>(x, dtype, n, d, dp, o0, o1, norms, row0);
+  else if (storage == FK_F16)
+    prep_rows_kernel<1><<<grid, wpb * 32, 0, st>>>(x, dtype, n, d, dp, o0, o1, norms, row0);
+  else
+    prep_rows_kernel<2><<<grid, wpb * 32, 0, st>>>(x, dtype, n, d, dp, o0, o1, norms, row0);
+  CKL();
+  return FK_OK;
+}
+
+size_t dtype_bytes(int dtype) { return dtype == FK_F32 ? 4 : 2; }
+
+template <int MODE, int KQ, bool IP>
+int launch_fused_t(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0, const CUtensorMap& b1,
+                   const SearchParams& sp, int grid, int smem, cudaStream_t st) {
+  auto kern = fused_knn_kernel<MODE, KQ, IP>;
+  static int configured_smem = 0;  // per instantiation
+  if (configured_smem < smem) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+    configured_smem = SMEM_LIMIT;
+  }
+  kern<<<grid, NUM_THREADS, smem, st>>>(a0, a1, b0, b1, sp);
+  CKL();
+  return FK_OK;
+}
+
+template <int MODE, bool IP>
+int launch_fused_k(int kq, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
+                   const CUtensorMap& b1, const SearchParams& sp, int grid, int smem, cudaStream_t st) {
+  switch (kq) {
+    case 8: return launch_fused_t<MODE, 8, IP>(a0, a1, b0, b1, sp, grid, smem, st);
+    case 16: return launch_fused_t<MODE, 16, IP>(a0, a1, b0, b1, sp, grid, smem, st);
+    case 32: return launch_fused_t<MODE, 32, IP>(a0, a1, b0, b1, sp, grid, smem, st);
+  }
+  return set_err(FK_E_UNSUPPORTED, "queue bucket %d", kq);
+}
+
+int launch_fused(int storage, bool ip, int kq, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
+                 const CUtensorMap& b1, const SearchParams& sp, int grid, int smem, cudaStream_t st) {
+  if (storage == FK_F32)
+    return ip ? launch_fused_k<0, true>(kq, a0, a1, b0, b1, sp, grid, smem, st)
+              : launch_fused_k<0, false>(kq, a0, a1, b0, b1, sp, grid, smem, st);
+  if (storage == FK_F16)
+    return ip ? launch_fused_k<1, true>(kq, a0, a1, b0, b1, sp, grid, smem, st)
+              : launch_fused_k<1, false>(kq, a0, a1, b0, b1, sp, grid, smem, st);
+  return ip ? launch_fused_k<2, true>(kq, a0, a1, b0, b1, sp, grid, smem, st)
+            : launch_fused_k<2, false>(kq, a0, a1, b0, b1, sp, grid, smem, st);
+}
+
+// Split-N plan: choose the number of N-chunks S so that num_m*S work units
+// spread evenly over the persistent grid (each unit = one 128-query tile x
+// one contiguous range of base tiles).  Units are ordered chunk-major, so the
+// CTAs resident at any moment stream the same ~2 chunks of the base through
+// L2 (the base is read from HBM about once per wave).
+void plan_split(int num_m, int n_tiles, int num_sms, int* S_out, int* chunk_out) {
+  double best_cost = 1e300;
+  int bestS = 1, bestC = n_tiles;
+  const double ovh = 1.5;  // per-unit cost in tile-equivalents (A reload, pipeline fill, flush)
+  const int smax = std::min(128, n_tiles);
+  for (int S = 1; S <= smax; ++S) {
+    const int chunk = (n_tiles + S - 1) / S;
+    const int s_eff = (n_tiles + chunk - 1) / chunk;
+    if (s_eff != S) continue;
+    const long units = (long)num_m * S;
+    const long grid = std::min<long>(units, num_sms);
+    const long waves = (units + grid - 1) / grid;
+    const double cost = (double)waves * (chunk + ovh) * ((double)num_sms / grid) + 1e-4 * S;
+    if (cost < best_cost) {
+      best_cost = cost;
+      bestS = S;
+      bestC = chunk;
+    }
+  }
+  *S_out = bestS;
+  *chunk_out = bestC;
+}
+
+}  // namespace
+
+// =====================================================================  C ABI
+extern "C" {
+
+const char* fk_last_error(void) { return g_err.c_str(); }
+
+int fk_create(int device, int d, int metric, int storage, fk_index** out) {
+  if (!out) return set_err(FK_E_INVALID, "out is NULL");
+  *out = nullptr;
+  if (d < 1) return set_err(FK_E_INVALID, "d must be >= 1");
+  if (metric != FK_METRIC_L2 && metric != FK_METRIC_IP)
+    return set_err(FK_E_UNSUPPORTED, "metric %d not supported by the GPU flat index (L2=1, IP=0)", metric);
+  if (storage != FK_F32 && storage != FK_F16 && storage != FK_BF16)
+    return set_err(FK_E_INVALID, "unknown storage %d", storage);
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return set_err(FK_E_INVALID, "device %d out of range (%d devices)", device, ndev);
+  CK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return set_err(FK_E_UNSUPPORTED, "device %d is sm_%d%d; this build targets sm_100a (B200)", device, prop.major,
+                   prop.minor);
+  fk_index* h = new fk_index();
+  h->device = device;
+  h->d = d;
+  const int ce = chunk_elems_of(storage);
+  h->dp = (d + ce - 1) / ce * ce;
+  h->metric = metric;
+  h->storage = storage;
+  h->num_sms = prop.multiProcessorCount;
+  if (const char* e = getenv("FK_NUM_SMS")) h->num_sms = std::max(1, std::min(atoi(e), h->num_sms));
+  *out = h;
+  return FK_OK;
+}
+
+void fk_destroy(fk_index* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  cudaDeviceSynchronize();
+  cudaFree(h->s0);
+  cudaFree(h->s1);
+  cudaFree(h->norms);
+  cudaFree(h->ids);
+  for (DevBuf* b : {&h->q_in, &h->q0, &h->q1, &h->qn, &h->pkey, &h->ppos, &h->outD, &h->outI, &h->outP,
+                    &h->stage_in, &h->stage_ids})
+    b->release();
+  for (auto& q : h->ev_pool)
+    for (auto& e : q) cudaEventDestroy(e);
+  delete h;
+}
+
+int64_t fk_ntotal(const fk_index* h) { return h ? h->ntotal : -1; }
+int fk_dim(const fk_index* h) { return h ? h->d : -1; }
+
+int fk_reset(fk_index* h) {
+  if (!h) return set_err(FK_E_INVALID, "NULL index");
+  std::lock_guard<std::mutex> g(h->mu);
+  h->ntotal = 0;
+  return FK_OK;
+}
+
+int fk_add(fk_index* h, const void* x, int64_t n, int dtype, const int64_t* ids, int on_device, void* stream) {
+  if (!h) return set_err(FK_E_INVALID, "NULL index");
+  if (n < 0) return set_err(FK_E_INVALID, "n must be >= 0");
+  if (dtype != FK_F32 && dtype != FK_F16 && dtype != FK_BF16) return set_err(FK_E_INVALID, "bad dtype %d", dtype);
+  if (n == 0) return FK_OK;
+  if (!x) return set_err(FK_E_INVALID, "x is NULL");
+  if (h->ntotal + n >= (int64_t)0xFFFFFFFFll)
+    return set_err(FK_E_UNSUPPORTED, "a single index holds < 2^32 vectors (positions are 32-bit, core.py:219)");
+  std::lock_guard<std::mutex> g(h->mu);
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int rc = grow(h, h->ntotal + n, st);
+  if (rc) return rc;
+  const size_t eb = dtype_bytes(dtype);
+  const size_t in_row = (size_t)h->d * eb;
+  // stage host input in <= 256 MB slices
+  const int64_t slice = on_device ? n : std::max<int64_t>(1, (int64_t)((256ull << 20) / in_row));
+  for (int64_t r0 = 0; r0 < n; r0 += slice) {
+    const int64_t m = std::min(slice, n - r0);
+    const void* src = static_cast<const uint8_t*>(x) + (size_t)r0 * in_row;
+    if (!on_device) {
+      if ((rc = h->stage_in.ensure(m * in_row))) return rc;
+      CK(cudaMemcpyAsync(h->stage_in.p, src, m * in_row, cudaMemcpyHostToDevice, st));
+      src = h->stage_in.p;
+    }
+    if ((rc = launch_prep(h->storage, src, dtype, m, h->d, h->dp, h->s0, h->s1, h->norms, h->ntotal + r0, st)))
+      return rc;
+    if (!on_device) CK(cudaStreamSynchronize(st));  // stage buffer reused by the next slice
+  }
+  if (ids) {
+    CK(cudaMemcpyAsync(h->ids + h->ntotal, ids, n * sizeof(int64_t),
+                       on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  } else {
+    iota_ids_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(h->ids + h->ntotal, h->ntotal, n);
+    CKL();
+  }
+  if (!on_device) CK(cudaStreamSynchronize(st));
+  h->ntotal += n;
+  return FK_OK;
+}
+
+int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D, int64_t* I, int64_t* P,
+              int on_device, void* stream) {
+  if (!h) return set_err(FK_E_INVALID, "NULL index");
+  if (k < 1) return set_err(FK_E_INVALID, "k must be >= 1");
+  if (nq < 0) return set_err(FK_E_INVALID, "nq must be >= 0");
+  if (dtype != FK_F32 && dtype != FK_F16 && dtype != FK_BF16) return set_err(FK_E_INVALID, "bad dtype %d", dtype);
+  if (nq == 0) return FK_OK;
+  if (!q || !D || !I) return set_err(FK_E_INVALID, "NULL query/output pointer");
+  if (nq > (int64_t)INT32_MAX / 2) return set_err(FK_E_UNSUPPORTED, "nq too large for one call");
+  std::lock_guard<std::mutex> g(h->mu);
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool ip = h->metric == FK_METRIC_IP;
+  const size_t nout = (size_t)nq * k;
+  int rc;
+  h->nlaunch = 0;
+  cudaEvent_t* ev = nullptr;
+  if (h->profiling && h->ntotal > 0 && !(ev = next_events(h))) return set_err(FK_E_CUDA, "cudaEventCreate failed");
+
+  float* dD = D;
+  int64_t* dI = I;
+  int64_t* dP = P;
+  if (!on_device) {
+    if ((rc = h->outD.ensure(nout * sizeof(float)))) return rc;
+    if ((rc = h->outI.ensure(nout * sizeof(int64_t)))) return rc;
+    dD = static_cast<float*>(h->outD.p);
+    dI = static_cast<int64_t*>(h->outI.p);
+    if (P) {
+      if ((rc = h->outP.ensure(nout * sizeof(int64_t)))) return rc;
+      dP = static_cast<int64_t*>(h->outP.p);
+    }
+  }
+
+  if (h->ntotal == 0) {  // flat.py:70-71: all-sentinel rows
+    fill_sentinel_kernel<<<(unsigned)((nout + 255) / 256), 256, 0, st>>>(dD, dI, dP, nout,
+                                                                         ip ? -INFINITY : INFINITY);
+    CKL();
+    h->nlaunch = 1;
+  } else {
+    int kq;
+    if (k <= 8) kq = 8;
+    else if (k <= 16) kq = 16;
+    else if (k <= 32) kq = 32;
+    else return set_err(FK_E_UNSUPPORTED, "k=%d: the large-k selection path is not built yet (k <= 32)", k);
+
+    // ---- queries -> device operand layout + norms
+    const size_t in_row = (size_t)h->d * dtype_bytes(dtype);
+    const void* qsrc = q;
+    if (!on_device) {
+      if ((rc = h->q_in.ensure(nq * in_row))) return rc;
+      CK(cudaMemcpyAsync(h->q_in.p, q, nq * in_row, cudaMemcpyHostToDevice, st));
+      qsrc = h->q_in.p;
+    }
+    const size_t qrow = row_bytes(h);
+    if ((rc = h->q0.ensure(nq * qrow))) return rc;
+    if (h->storage == FK_F32 && (rc = h->q1.ensure(nq * qrow))) return rc;
+    if ((rc = h->qn.ensure(nq * sizeof(float)))) return rc;
+    if (ev) CK(cudaEventRecord(ev[0], st));
+    if ((rc = launch_prep(h->storage, qsrc, dtype, nq, h->d, h->dp, h->q0.p, h->q1.p, static_cast<float*>(h->qn.p),
+                          0, st)))
+      return rc;
+    h->nlaunch++;
+
+    // ---- plan
+    const int num_m = (int)((nq + BM - 1) / BM);
+    const int n_tiles = (int)((h->ntotal + BN - 1) / BN);
+    int S, chunk_tiles;
+    plan_split(num_m, n_tiles, h->num_sms, &S, &chunk_tiles);
+    if (const char* e = getenv("FK_FORCE_S")) {
+      S = std::max(1, std::min(atoi(e), std::min(128, n_tiles)));
+      chunk_tiles = (n_tiles + S - 1) / S;
+      S = (n_tiles + chunk_tiles - 1) / chunk_tiles;
+    }
+    const int num_units = num_m * S;
+    const int grid = std::min(num_units, h->num_sms);
+    const int split = split_of(h->storage);
+    const int num_kb = h->dp / chunk_elems_of(h->storage);
+    const int a_bytes = split * num_kb * (int)CHUNK_BYTES;
+    int a_res = 1;
+    int stages = (SMEM_LIMIT - SMEM_RESERVE - a_bytes) / (split * (int)CHUNK_BYTES);
+    if (stages < 3) {
+      a_res = 0;
+      stages = (SMEM_LIMIT - SMEM_RESERVE) / (2 * split * (int)CHUNK_BYTES);
+    }
+    stages = std::min(stages, 8);
+    if (stages < 2) return set_err(FK_E_UNSUPPORTED, "pipeline does not fit in shared memory");
+    if (const char* e = getenv("FK_FORCE_STREAM_A")) {
+      if (atoi(e)) {
+        a_res = 0;
+        stages = std::min(8, (SMEM_LIMIT - SMEM_RESERVE) / (2 * split * (int)CHUNK_BYTES));
+      }
+    }
+    const int smem = SMEM_RESERVE + (a_res ? a_bytes : 0) + stages * (a_res ? 1 : 2) * split * (int)CHUNK_BYTES;
+
+    if ((rc = h->pkey.ensure((size_t)nq * S * k * sizeof(uint32_t)))) return rc;
+    if ((rc = h->ppos.ensure((size_t)nq * S * k * sizeof(uint32_t)))) return rc;
+
+    CUtensorMap ta0, ta1, tb0, tb1;
+    const int eb = elem_bytes_of(h->storage);
+    if ((rc = make_map(&ta0, h->q0.p, eb, h->dp, nq))) return rc;
+    if ((rc = make_map(&tb0, h->s0, eb, h->dp, h->ntotal))) return rc;
+    if (h->storage == FK_F32) {
+      if ((rc = make_map(&ta1, h->q1.p, eb, h->dp, nq))) return rc;
+      if ((rc = make_map(&tb1, h->s1, eb, h->dp, h->ntotal))) return rc;
+    } else {
+      ta1 = ta0;
+      tb1 = tb0;
+    }
+    SearchParams sp;
+    sp.qnorm = static_cast<const float*>(h->qn.p);
+    sp.xnorm = h->norms;
+    sp.part_key = static_cast<uint32_t*>(h->pkey.p);
+    sp.part_pos = static_cast<uint32_t*>(h->ppos.p);
+    sp.dbg_ip = h->dbg_ip;
+    sp.nq = (int)nq;
+    sp.nb = (int)h->ntotal;
+    sp.k = k;
+    sp.num_m = num_m;
+    sp.n_tiles = n_tiles;
+    sp.chunk_tiles = chunk_tiles;
+    sp.S = S;
+    sp.num_units = num_units;
+    sp.num_kb = num_kb;
+    sp.a_resident = a_res;
+    sp.stages = stages;
+    h->plan[0] = grid;
+    h->plan[1] = S;
+    h->plan[2] = chunk_tiles;
+    h->plan[3] = num_units;
+    h->plan[4] = stages;
+    h->plan[5] = a_res;
+    h->plan[6] = smem;
+    h->plan[7] = kq;
+
+    if (ev) CK(cudaEventRecord(ev[1], st));
+    if ((rc = launch_fused(h->storage, ip, kq, ta0, ta1, tb0, tb1, sp, grid, smem, st))) return rc;
+    h->nlaunch++;
+    if (ev) CK(cudaEventRecord(ev[2], st));
+
+    const int wpb = 8;
+    const unsigned mgrid = (unsigned)((nq + wpb - 1) / wpb);
+    if (ip)
+      merge_kernel<true><<<mgrid, wpb * 32, 0, st>>>(sp.part_key, sp.part_pos, S, (int)nq, k, h->ids, dD, dI, dP);
+    else
+      merge_kernel<false><<<mgrid, wpb * 32, 0, st>>>(sp.part_key, sp.part_pos, S, (int)nq, k, h->ids, dD, dI, dP);
+    CKL();
+    h->nlaunch++;
+    if (ev) CK(cudaEventRecord(ev[3], st));
+  }
+
+  if (!on_device) {
+    CK(cudaMemcpyAsync(D, dD, nout * sizeof(float), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(I, dI, nout * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    if (P) CK(cudaMemcpyAsync(P, dP, nout * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  h->nlaunch_acc += h->nlaunch;
+  return FK_OK;
+}
+
+int fk_merge_shards(int metric, int nshard, int64_t nq, int k, const float* D_in, const int64_t* P_in,
+                    const int64_t* I_in, float* D_out, int64_t* I_out, void* stream) {
+  if (nshard < 1 || nshard > 64) return set_err(FK_E_INVALID, "nshard must be in [1, 64]");
+  if (k < 1 || nq < 0) return set_err(FK_E_INVALID, "bad k / nq");
+  if (nq == 0) return FK_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int wpb = 8;
+  const unsigned grid = (unsigned)((nq + wpb - 1) / wpb);
+  if (metric == FK_METRIC_IP)
+    shard_merge_kernel<true><<<grid, wpb * 32, 0, st>>>(nshard, (int)nq, k, D_in, P_in, I_in, D_out, I_out);
+  else
+    shard_merge_kernel<false><<<grid, wpb * 32, 0, st>>>(nshard, (int)nq, k, D_in, P_in, I_in, D_out, I_out);
+  CKL();
+  return FK_OK;
+}
+
+int fk_reconstruct(fk_index* h, const int64_t* positions, int64_t n, float* out, int on_device, void* stream) {
+  if (!h) return set_err(FK_E_INVALID, "NULL index");
+  if (n <= 0) return FK_OK;
+  std::lock_guard<std::mutex> g(h->mu);
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int rc;
+  const int64_t* dpos = positions;
+  float* dout = out;
+  if (!on_device) {
+    std::vector<int64_t> chk(positions, positions + n);
+    for (int64_t p : chk)
+      if (p < 0 || p >= h->ntotal) return set_err(FK_E_INVALID, "position %lld out of range", (long long)p);
+    if ((rc = h->stage_ids.ensure(n * sizeof(int64_t)))) return rc;
+    if ((rc = h->stage_in.ensure(n * (size_t)h->d * sizeof(float)))) return rc;
+    CK(cudaMemcpyAsync(h->stage_ids.p, positions, n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    dpos = static_cast<const int64_t*>(h->stage_ids.p);
+    dout = static_cast<float*>(h->stage_in.p);
+  }
+  const unsigned grid = (unsigned)((n + 7) / 8);
+  if (h->storage == FK_F32) reconstruct_kernel<0><<<grid, 256, 0, st>>>(h->s0, h->s1, h->dp, h->d, dpos, n, dout);
+  else if (h->storage == FK_F16) reconstruct_kernel<1><<<grid, 256, 0, st>>>(h->s0, h->s1, h->dp, h->d, dpos, n, dout);
+  else reconstruct_kernel<2><<<grid, 256, 0, st>>>(h->s0, h->s1, h->dp, h->d, dpos, n, dout);
+  CKL();
+  if (!on_device) {
+    CK(cudaMemcpyAsync(out, dout, n * (size_t)h->d * sizeof(float), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  return FK_OK;
+}
+
+int fk_get_ids(fk_index* h, int64_t* out_host) {
+  if (!h) return set_err(FK_E_INVALID, "NULL index");
+  std::lock_guard<std::mutex> g(h->mu);
+  CK(cudaSetDevice(h->device));
+  if (h->ntotal) CK(cudaMemcpy(out_host, h->ids, h->ntotal * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  return FK_OK;
+}
+
+int fk_remove_ids(fk_index* h, const int64_t* ids, int64_t n, int on_device, int64_t* removed, void* stream) {
+  if (!h) return set_err(FK_E_INVALID, "NULL index");
+  if (removed) *removed = 0;
+  if (n <= 0 || h->ntotal == 0) return FK_OK;
+  std::lock_guard<std::mutex> g(h->mu);
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  std::vector<int64_t> del(n), cur(h->ntotal);
+  CK(cudaMemcpyAsync(del.data(), ids, n * sizeof(int64_t), on_device ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost,
+                     st));
+  CK(cudaMemcpyAsync(cur.data(), h->ids, h->ntotal * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::unordered_set<int64_t> kill(del.begin(), del.end());
+  std::vector<int64_t> keep;
+  keep.reserve(h->ntotal);
+  for (int64_t i = 0; i < h->ntotal; ++i)
+    if (!kill.count(cur[i])) keep.push_back(i);
+  const int64_t nrem = h->ntotal - (int64_t)keep.size();
+  if (removed) *removed = nrem;
+  if (nrem == 0) return FK_OK;
+  const int64_t nk = (int64_t)keep.size();
+  int rc;
+  if (nk > 0) {
+    if ((rc = h->stage_ids.ensure(nk * sizeof(int64_t)))) return rc;
+    CK(cudaMemcpyAsync(h->stage_ids.p, keep.data(), nk * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    const int64_t* dkeep = static_cast<const int64_t*>(h->stage_ids.p);
+    const size_t rb = row_bytes(h);
+    // compact every column of the store through a scratch buffer (order preserved, flat.py:50-53)
+    struct Col {
+      void* p;
+      size_t rb;
+    } cols[4] = {{h->s0, rb}, {h->s1, rb}, {h->norms, sizeof(float)}, {h->ids, sizeof(int64_t)}};
+    for (auto& c : cols) {
+      if (!c.p) continue;
+      if ((rc = h->stage_in.ensure(nk * c.rb))) return rc;
+      gather_rows_kernel<<<(unsigned)nk, 128, 0, st>>>(static_cast<const uint8_t*>(c.p),
+                                                        static_cast<uint8_t*>(h->stage_in.p), c.rb, dkeep, nk);
+      CKL();
+      CK(cudaMemcpyAsync(c.p, h->stage_in.p, nk * c.rb, cudaMemcpyDeviceToDevice, st));
+    }
+    CK(cudaStreamSynchronize(st));
+  }
+  h->ntotal = nk;
+  return FK_OK;
+}
+
+int fk_set_profiling(fk_index* h, int on) {
+  if (!h) return set_err(FK_E_INVALID, "NULL index");
+  h->profiling = on;
+  return FK_OK;
+}
+
+int fk_kernel_times(fk_index* h, float* ms3, int* nlaunch) {
+  if (!h) return set_err(FK_E_INVALID, "NULL index");
+  std::lock_guard<std::mutex> g(h->mu);
+  CK(cudaSetDevice(h->device));
+  double acc[3] = {0, 0, 0};
+  for (size_t i = 0; i < h->ev_used; ++i) {
+    auto& q = h->ev_pool[i];
+    CK(cudaEventSynchronize(q[3]));
+    for (int j = 0; j < 3; ++j) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, q[j], q[j + 1]));
+      acc[j] += ms;
+    }
+  }
+  if (ms3)
+    for (int j = 0; j < 3; ++j) ms3[j] = h->ev_used ? (float)(acc[j] / h->ev_used) : 0.f;
+  if (nlaunch) *nlaunch = (int)h->nlaunch_acc;
+  h->ev_used = 0;
+  h->nlaunch_acc = 0;
+  return FK_OK;
+}
+
+int fk_last_plan(fk_index* h, int* out8) {
+  if (!h || !out8) return set_err(FK_E_INVALID, "NULL argument");
+  std::memcpy(out8, h->plan, sizeof(h->plan));
+  return FK_OK;
+}
+
+// Test hook (not in the public header): route raw inner products of the next
+// searches to a caller-owned device buffer [nq][ntotal] (NULL disables).
+int fk_debug_set_ip_dump(fk_index* h, float* dev_buf) {
+  if (!h) return set_err(FK_E_INVALID, "NULL index");
+  h->dbg_ip = dev_buf;
+  return FK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,533 @@
+// Device kernels of the B200-native exact flat k-NN engine.
+//
+//   prep_rows_kernel   : f32/f16/bf16 rows -> stored operand layout
+//                        (3xTF32 hi/lo split or RNE fp16/bf16) + fp32 norms.
+//                        Base side = FlatIndex._add + norms einsum
+//                        (reference flat.py:28-32); query side = the qn einsum
+//                        of flat_search_blas (flat.py:110).
+//   fused_knn_kernel   : persistent, warp-specialised tcgen05 GEMM
+//                        (TMA -> smem -> tcgen05.mma -> TMEM) with the L2/IP
+//                        epilogue (flat.py:108-114) and the per-row top-k
+//                        selection (core.py:205-236) fused behind it, so the
+//                        nq x nb distance matrix never reaches HBM.
+//   merge_kernel       : split-N partial lists -> final top-k, position -> id
+//                        (flat.py:68-73).
+//   shard_merge_kernel : per-shard top-k lists -> single-index order (8(e)).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "sm100.cuh"
+
+namespace fk {
+
+constexpr int BM = 128;                        // queries per tile (TMEM lanes)
+constexpr int BN = 128;                        // base rows per tile (TMEM columns)
+constexpr uint32_t CHUNK_BYTES = 128u * 128u;  // one 128-row x 128-byte K-chunk
+constexpr int TMEM_COLS = 2 * BN;              // double-buffered accumulator
+constexpr int NUM_THREADS = 256;               // 4 control warps + 4 epilogue warps
+constexpr int EPI_WARP0 = 4;
+
+// ------------------------------------------------------------ key helpers
+// Order-preserving float32 -> uint32 (core.py:193-197): NaN above +inf,
+// -0.0 below +0.0.  Comparing (key, position) reproduces the reference's
+// 64-bit composite sort key (core.py:219).
+__device__ __forceinline__ uint32_t monotone(float f) {
+  const uint32_t b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float unmonotone(uint32_t k) {
+  const uint32_t b = (k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k;
+  return __uint_as_float(b);
+}
+
+struct SearchParams {
+  const float* qnorm;  // [nq]
+  const float* xnorm;  // [cap], cap padded to BN
+  uint32_t* part_key;  // [nq][S][k]
+  uint32_t* part_pos;  // [nq][S][k]
+  float* dbg_ip;       // optional raw inner products [nq][nb] (debug)
+  int nq, nb, k;
+  int num_m, n_tiles, chunk_tiles, S, num_units;
+  int num_kb;      // padded d / elements-per-128B-chunk
+  int a_resident;  // queries kept in smem for a whole work unit
+  int stages;      // B (and streamed A) pipeline depth
+};
+
+// ------------------------------------------------------------ register queue
+// Sorted ascending (worst at KQ-1).  Slots [0, KQ-k) hold phantom key 0 which
+// nothing displaces, so a runtime k <= KQ needs only static register indices.
+// Ties: a new candidate always has a larger position than every queued one
+// (columns are streamed in order), so strict `<` keeps the smaller position
+// first -- the reference's (value, column) order.
+template <int KQ>
+__device__ __forceinline__ void queue_insert(uint32_t (&keys)[KQ], uint32_t (&pos)[KQ], uint32_t key,
+                                             uint32_t p) {
+  if (key < keys[KQ - 1]) {
+#pragma unroll
+    for (int i = KQ - 1; i > 0; --i) {
+      const bool shift = key < keys[i - 1];
+      const uint32_t nk = shift ? keys[i - 1] : key;
+      const uint32_t np = shift ? pos[i - 1] : p;
+      if (key < keys[i]) {
+        keys[i] = nk;
+        pos[i] = np;
+      }
+    }
+    if (key < keys[0]) {
+      keys[0] = key;
+      pos[0] = p;
+    }
+  }
+}
+
+// ------------------------------------------------------------ fused kernel
+// MODE 0: fp32 storage, 3xTF32 (A_hi.B_hi + A_hi.B_lo + A_lo.B_hi)
+// MODE 1: fp16, MODE 2: bf16 (single kind::f16 pass)
+template <int MODE, int KQ, bool IS_IP>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    fused_knn_kernel(const __grid_constant__ CUtensorMap tm_a0, const __grid_constant__ CUtensorMap tm_a1,
+                     const __grid_constant__ CUtensorMap tm_b0, const __grid_constant__ CUtensorMap tm_b1,
+                     const SearchParams p) {
+  constexpr int SPLIT = (MODE == 0) ? 2 : 1;
+  constexpr int BK = (MODE == 0) ? 32 : 64;  // elements per 128-byte K-chunk
+  constexpr uint32_t AB_FMT = (MODE == 0) ? 2u : (MODE == 1 ? 0u : 1u);
+  constexpr uint32_t IDESC = make_idesc(AB_FMT, BM, BN);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int num_kb = p.num_kb;
+  const int stages = p.stages;
+  const bool a_res = p.a_resident != 0;
+  const uint32_t a_bytes = a_res ? SPLIT * num_kb * CHUNK_BYTES : 0u;
+  const uint32_t stage_bytes = (a_res ? SPLIT : 2 * SPLIT) * CHUNK_BYTES;
+
+  uint8_t* a_region = smem;
+  uint8_t* st_region = smem + a_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(st_region + stages * stage_bytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + stages;
+  uint64_t* tfull = bars + 2 * stages;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* afull = tempty + 2;
+  uint64_t* aempty = afull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 1);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_a0);
+    tma_prefetch_desc(&tm_b0);
+    if (SPLIT == 2) {
+      tma_prefetch_desc(&tm_a1);
+      tma_prefetch_desc(&tm_b1);
+    }
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);  // one arrival per epilogue warp
+    }
+    mbar_init(afull, 1);
+    mbar_init(aempty, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      const uint64_t pol_a = policy_evict_last();
+      const uint64_t pol_b = policy_evict_first();
+      uint32_t stage = 0, phase = 0;
+      int j = 0;
+      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++j) {
+        const int chunk = u / p.num_m;
+        const int m = u - chunk * p.num_m;
+        const int t0 = chunk * p.chunk_tiles;
+        const int t1 = min(t0 + p.chunk_tiles, p.n_tiles);
+        if (a_res) {
+          if (j > 0) mbar_wait(aempty, (j - 1) & 1);
+          mbar_arrive_expect_tx(afull, a_bytes);
+          for (int part = 0; part < SPLIT; ++part)
+            for (int kb = 0; kb < num_kb; ++kb)
+              tma_load_2d(a_region + (part * num_kb + kb) * CHUNK_BYTES, part ? &tm_a1 : &tm_a0, afull,
+                          kb * BK, m * BM, pol_a);
+        }
+        for (int t = t0; t < t1; ++t) {
+          for (int kb = 0; kb < num_kb; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_arrive_expect_tx(&full[stage], stage_bytes);
+            uint8_t* sb = st_region + stage * stage_bytes;
+            for (int part = 0; part < SPLIT; ++part)
+              tma_load_2d(sb + part * CHUNK_BYTES, part ? &tm_b1 : &tm_b0, &full[stage], kb * BK, t * BN, pol_b);
+            if (!a_res)
+              for (int part = 0; part < SPLIT; ++part)
+                tma_load_2d(sb + (SPLIT + part) * CHUNK_BYTES, part ? &tm_a1 : &tm_a0, &full[stage], kb * BK,
+                            m * BM, pol_a);
+            if (++stage == (uint32_t)stages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (single thread) =====================
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0, tcount = 0;
+      int j = 0;
+      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++j) {
+        const int chunk = u / p.num_m;
+        const int t0 = chunk * p.chunk_tiles;
+        const int t1 = min(t0 + p.chunk_tiles, p.n_tiles);
+        if (a_res) {
+          mbar_wait(afull, j & 1);
+          tc_fence_after();
+        }
+        for (int t = t0; t < t1; ++t, ++tcount) {
+          const uint32_t buf = tcount & 1, tph = (tcount >> 1) & 1;
+          mbar_wait(&tempty[buf], tph ^ 1);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + buf * BN;
+          for (int kb = 0; kb < num_kb; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            uint8_t* sb = st_region + stage * stage_bytes;
+            const uint8_t* a0 = a_res ? a_region + kb * CHUNK_BYTES : sb + SPLIT * CHUNK_BYTES;
+            const uint64_t ad0 = smem_desc_sw128(smem_u32(a0));
+            const uint64_t bd0 = smem_desc_sw128(smem_u32(sb));
+            if (MODE == 0) {
+              const uint8_t* a1 = a_res ? a_region + (num_kb + kb) * CHUNK_BYTES : sb + 3 * CHUNK_BYTES;
+              const uint64_t ad1 = smem_desc_sw128(smem_u32(a1));
+              const uint64_t bd1 = smem_desc_sw128(smem_u32(sb + CHUNK_BYTES));
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk) {
+                const uint64_t off = 2 * kk;  // 32 bytes per K=8 tf32 step, in 16-byte units
+                mma_tf32(d_tmem, ad1 + off, bd0 + off, IDESC, (kb | kk) != 0);  // lo * hi
+                mma_tf32(d_tmem, ad0 + off, bd1 + off, IDESC, 1u);              // hi * lo
+                mma_tf32(d_tmem, ad0 + off, bd0 + off, IDESC, 1u);              // hi * hi
+              }
+            } else {
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk) {
+                const uint64_t off = 2 * kk;  // 32 bytes per K=16 f16 step
+                mma_f16(d_tmem, ad0 + off, bd0 + off, IDESC, (kb | kk) != 0);
+              }
+            }
+            mma_commit(&empty[stage]);
+            if (++stage == (uint32_t)stages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          mma_commit(&tfull[buf]);
+        }
+        if (a_res) mma_commit(aempty);
+      }
+    }
+  } else if (warp >= EPI_WARP0) {
+    // ===================== epilogue: TMEM -> distances -> top-k =====================
+    const int eq = warp & 3;  // TMEM lane quarter this warp may access
+    const uint32_t lane_addr = static_cast<uint32_t>(eq * 32) << 16;
+    const int k = p.k;
+    uint32_t tcount = 0;
+    for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+      const int chunk = u / p.num_m;
+      const int m = u - chunk * p.num_m;
+      const int t0 = chunk * p.chunk_tiles;
+      const int t1 = min(t0 + p.chunk_tiles, p.n_tiles);
+      const int row = m * BM + eq * 32 + lane;
+      const bool row_ok = row < p.nq;
+      const float qn = (!IS_IP && row_ok) ? p.qnorm[row] : 0.f;
+
+      uint32_t keys[KQ], pos[KQ];
+#pragma unroll
+      for (int i = 0; i < KQ; ++i) {
+        keys[i] = (i < KQ - k) ? 0u : 0xFFFFFFFFu;
+        pos[i] = 0xFFFFFFFFu;
+      }
+      float thr = __uint_as_float(0x7FFFFFFFu);  // NaN: queue not full, everything passes
+
+      for (int t = t0; t < t1; ++t, ++tcount) {
+        const uint32_t buf = tcount & 1, tph = (tcount >> 1) & 1;
+        mbar_wait(&tfull[buf], tph);
+        tc_fence_after();
+        const int n0 = t * BN;
+        const int nvalid = p.nb - n0;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tmem_base + lane_addr + buf * BN + c * 32, r);
+          tmem_ld_wait();
+          if (p.dbg_ip != nullptr && row_ok) {
+            for (int j = 0; j < 32; ++j)
+              if (c * 32 + j < nvalid)
+                p.dbg_ip[(size_t)row * p.nb + n0 + c * 32 + j] = __uint_as_float(r[j]);
+          }
+          const float4* xn4 = reinterpret_cast<const float4*>(p.xnorm + n0 + c * 32);
+#pragma unroll
+          for (int j4 = 0; j4 < 8; ++j4) {
+            float xs[4] = {0.f, 0.f, 0.f, 0.f};
+            if (!IS_IP) {
+              const float4 v = __ldg(xn4 + j4);
+              xs[0] = v.x;
+              xs[1] = v.y;
+              xs[2] = v.z;
+              xs[3] = v.w;
+            }
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+              const int j = j4 * 4 + jj;
+              const float ip = __uint_as_float(r[j]);
+              // flat.py:111: dmat = (qn + norms) - 2.0*ip  (2*ip exact -> one FMA)
+              float s = IS_IP ? -ip : fmaf(-2.f, ip, qn + xs[jj]);
+              if (!(s > thr)) {
+                const int col = c * 32 + j;
+                if (col < nvalid) {
+                  if (!IS_IP) s = (s <= 0.f) ? 0.f : s;  // np.maximum(dmat, 0) (flat.py:112)
+                  queue_insert<KQ>(keys, pos, monotone(s), static_cast<uint32_t>(n0 + col));
+                  thr = unmonotone(keys[KQ - 1]);
+                }
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
+      }
+      if (row_ok) {
+        const size_t base = ((size_t)row * p.S + chunk) * (size_t)k;
+#pragma unroll
+        for (int i = 0; i < KQ; ++i) {
+          if (i >= KQ - k) {
+            p.part_key[base + i - (KQ - k)] = keys[i];
+            p.part_pos[base + i - (KQ - k)] = pos[i];
+          }
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------ merges
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const uint64_t o = __shfl_xor_sync(0xFFFFFFFFu, v, off);
+    v = o < v ? o : v;
+  }
+  return v;
+}
+
+// One warp per query: k rounds of a warp-wide argmin over the heads of S
+// sorted partial lists (lane l owns lists l, l+32, l+64, l+96 -> S <= 128).
+template <bool IS_IP>
+__global__ void merge_kernel(const uint32_t* __restrict__ pkey, const uint32_t* __restrict__ ppos, int S, int nq,
+                             int k, const int64_t* __restrict__ ids, float* __restrict__ D,
+                             int64_t* __restrict__ I, int64_t* __restrict__ P) {
+  const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (q >= nq) return;
+  const uint32_t* lk = pkey + (size_t)q * S * k;
+  const uint32_t* lp = ppos + (size_t)q * S * k;
+  int h0 = 0, h1 = 0, h2 = 0, h3 = 0;
+  auto head = [&](int i, int h) -> uint64_t {
+    const int l = lane + 32 * i;
+    if (l >= S || h >= k) return ~0ull;
+    const size_t o = (size_t)l * k + h;
+    return (static_cast<uint64_t>(lk[o]) << 32) | lp[o];
+  };
+  uint64_t c0 = head(0, 0), c1 = head(1, 0), c2 = head(2, 0), c3 = head(3, 0);
+  for (int r = 0; r < k; ++r) {
+    uint64_t best = c0;
+    int bi = 0;
+    if (c1 < best) { best = c1; bi = 1; }
+    if (c2 < best) { best = c2; bi = 2; }
+    if (c3 < best) { best = c3; bi = 3; }
+    const uint64_t w = warp_min_u64(best);
+    if (w != ~0ull && best == w) {
+      if (bi == 0) c0 = head(0, ++h0);
+      else if (bi == 1) c1 = head(1, ++h1);
+      else if (bi == 2) c2 = head(2, ++h2);
+      else c3 = head(3, ++h3);
+    }
+    if (lane == 0) {
+      const size_t o = (size_t)q * k + r;
+      if (w == ~0ull) {
+        D[o] = IS_IP ? -INFINITY : INFINITY;
+        I[o] = -1;
+        if (P) P[o] = -1;
+      } else {
+        const uint32_t key = static_cast<uint32_t>(w >> 32);
+        const uint32_t ps = static_cast<uint32_t>(w & 0xFFFFFFFFu);
+        const float v = unmonotone(key);
+        D[o] = IS_IP ? -v : v;
+        I[o] = ids[ps];
+        if (P) P[o] = ps;
+      }
+    }
+  }
+}
+
+// Shard merge: nshard lists per query of (D, global position, id), already
+// best-first.  Ordering by (monotone key, global position) reproduces the
+// unsharded reference order exactly.  Lane l owns shards l, l+32 (<= 64).
+template <bool IS_IP>
+__global__ void shard_merge_kernel(int nshard, int nq, int k, const float* __restrict__ Din,
+                                   const int64_t* __restrict__ Pin, const int64_t* __restrict__ Iin,
+                                   float* __restrict__ D, int64_t* __restrict__ I) {
+  const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (q >= nq) return;
+  auto head = [&](int s, int h, int64_t& id) -> uint64_t {
+    if (s >= nshard || h >= k) return ~0ull;
+    const size_t o = ((size_t)s * nq + q) * k + h;
+    const int64_t ps = Pin[o];
+    if (ps < 0) return ~0ull;
+    id = Iin[o];
+    const float v = Din[o];
+    return (static_cast<uint64_t>(monotone(IS_IP ? -v : v)) << 32) | static_cast<uint32_t>(ps);
+  };
+  int h0 = 0, h1 = 0;
+  int64_t id0 = -1, id1 = -1;
+  uint64_t c0 = head(lane, 0, id0), c1 = head(lane + 32, 0, id1);
+  for (int r = 0; r < k; ++r) {
+    const bool second = c1 < c0;
+    const uint64_t best = second ? c1 : c0;
+    const int64_t bid = second ? id1 : id0;
+    const uint64_t w = warp_min_u64(best);
+    const unsigned win = __ballot_sync(0xFFFFFFFFu, w != ~0ull && best == w);
+    int64_t wid = -1;
+    if (win) wid = __shfl_sync(0xFFFFFFFFu, bid, __ffs(win) - 1);
+    if (w != ~0ull && best == w) {
+      if (second) c1 = head(lane + 32, ++h1, id1);
+      else c0 = head(lane, ++h0, id0);
+    }
+    if (lane == 0) {
+      const size_t o = (size_t)q * k + r;
+      if (w == ~0ull) {
+        D[o] = IS_IP ? -INFINITY : INFINITY;
+        I[o] = -1;
+      } else {
+        const float v = unmonotone(static_cast<uint32_t>(w >> 32));
+        D[o] = IS_IP ? -v : v;
+        I[o] = wid;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------ conversions
+__device__ __forceinline__ float load_elem(const void* x, int dtype, size_t i) {
+  if (dtype == 0) return static_cast<const float*>(x)[i];
+  if (dtype == 1) return __half2float(static_cast<const __half*>(x)[i]);
+  return __bfloat162float(static_cast<const __nv_bfloat16*>(x)[i]);
+}
+__device__ __forceinline__ float tf32_rna(float v) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+  return __uint_as_float(r);
+}
+
+// One warp per row: convert n rows of `x` (row-major n x d, dtype in_dtype)
+// into the stored layout at rows [row0, row0+n) of out0/out1 (dp columns,
+// zero padded), and write fp32 squared norms of the STORED values.
+template <int MODE>
+__global__ void prep_rows_kernel(const void* __restrict__ x, int in_dtype, int64_t n, int d, int dp,
+                                 void* __restrict__ out0, void* __restrict__ out1, float* __restrict__ norms,
+                                 int64_t row0) {
+  const int64_t rloc = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (rloc >= n) return;
+  const int64_t orow = row0 + rloc;
+  double acc = 0.0;
+  for (int c = lane; c < dp; c += 32) {
+    const float v = c < d ? load_elem(x, in_dtype, (size_t)rloc * d + c) : 0.f;
+    if (MODE == 0) {
+      const float hi = tf32_rna(v);
+      const float lo = v - hi;  // exact: x == hi + lo
+      static_cast<float*>(out0)[(size_t)orow * dp + c] = hi;
+      static_cast<float*>(out1)[(size_t)orow * dp + c] = lo;
+      acc += (double)v * (double)v;
+    } else if (MODE == 1) {
+      const __half h = __float2half_rn(v);
+      static_cast<__half*>(out0)[(size_t)orow * dp + c] = h;
+      const float vr = __half2float(h);
+      acc += (double)vr * (double)vr;
+    } else {
+      const __nv_bfloat16 h = __float2bfloat16_rn(v);
+      static_cast<__nv_bfloat16*>(out0)[(size_t)orow * dp + c] = h;
+      const float vr = __bfloat162float(h);
+      acc += (double)vr * (double)vr;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, off);
+  if (lane == 0 && norms != nullptr) norms[orow] = static_cast<float>(acc);
+}
+
+// Stored rows (by position) back to float32 n x d.
+template <int MODE>
+__global__ void reconstruct_kernel(const void* __restrict__ s0, const void* __restrict__ s1, int dp, int d,
+                                   const int64_t* __restrict__ positions, int64_t n, float* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const int64_t r = positions[i];
+  for (int c = lane; c < d; c += 32) {
+    float v;
+    if (MODE == 0)
+      v = static_cast<const float*>(s0)[(size_t)r * dp + c] + static_cast<const float*>(s1)[(size_t)r * dp + c];
+    else if (MODE == 1)
+      v = __half2float(static_cast<const __half*>(s0)[(size_t)r * dp + c]);
+    else
+      v = __bfloat162float(static_cast<const __nv_bfloat16*>(s0)[(size_t)r * dp + c]);
+    out[(size_t)i * d + c] = v;
+  }
+}
+
+// Gather rows (by position) of a row-major [*, row_bytes] buffer.
+__global__ void gather_rows_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, size_t row_bytes,
+                                   const int64_t* __restrict__ keep, int64_t n) {
+  const int64_t i = blockIdx.x;
+  if (i >= n) return;
+  const uint8_t* s = src + (size_t)keep[i] * row_bytes;
+  uint8_t* o = dst + (size_t)i * row_bytes;
+  for (size_t b = threadIdx.x * 4; b < row_bytes; b += blockDim.x * 4)
+    *reinterpret_cast<uint32_t*>(o + b) = *reinterpret_cast<const uint32_t*>(s + b);
+}
+
+__global__ void iota_ids_kernel(int64_t* ids, int64_t start, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) ids[i] = start + i;
+}
+
+__global__ void fill_sentinel_kernel(float* D, int64_t* I, int64_t* P, size_t n, float v) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    D[i] = v;
+    I[i] = -1;
+    if (P) P[i] = -1;
+  }
+}
+
+}  // namespace fk

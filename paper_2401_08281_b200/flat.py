@@ -1,0 +1,221 @@
+"""GPU FlatIndex: drop-in for the reference ``annkit.flat.FlatIndex`` (flat.py:14-65).
+
+Every search runs the sm_100a path through the C ABI (``include/flatknn.h``):
+query prep kernel -> fused tcgen05 GEMM + top-k kernel -> merge kernel.
+There is no CPU fallback and no nq-threshold dispatch: the reference's
+``nq < config.blas_threshold`` direct path (flat.py:58-62) exists only to
+avoid BLAS overhead on a CPU, and both of its paths compute the same exact
+top-k under the same (distance, position) order.
+
+Storage modes:
+  "fp32" -- fp32 vectors searched with a 3xTF32 split (fp32-faithful);
+  "fp16" / "bf16" -- vectors (and queries) rounded RNE to 16 bits, single
+  tensor-core pass; norms are computed from the rounded values, so results
+  equal the reference run on the same rounded inputs.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native as N
+from .core import METRIC_IP, METRIC_L2, Index, Metric, SearchResult, as_vectors, is_torch, metric_value
+
+try:
+    import torch
+except ImportError:  # pragma: no cover
+    torch = None
+
+_STORAGE = {"fp32": N.FK_F32, "float32": N.FK_F32, "fp16": N.FK_F16, "float16": N.FK_F16,
+            "bf16": N.FK_BF16, "bfloat16": N.FK_BF16}
+
+
+def _dtype_code(x) -> int:
+    if is_torch(x):
+        return {torch.float32: N.FK_F32, torch.float16: N.FK_F16, torch.bfloat16: N.FK_BF16}[x.dtype]
+    return {np.dtype(np.float32): N.FK_F32, np.dtype(np.float16): N.FK_F16}[x.dtype]
+
+
+def _ptr(x) -> int:
+    return x.data_ptr() if is_torch(x) else x.ctypes.data
+
+
+def _stream_of(device: int) -> int:
+    if torch is None or not torch.cuda.is_available():
+        return 0
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+class FlatIndex(Index):
+    """Exact k-NN over raw vectors stored in HBM (reference flat.py:14-26).
+
+    Parameters mirror the reference (``d``, ``metric``) plus the B200 storage
+    mode and the CUDA device ordinal.
+    """
+
+    def __init__(self, d: int, metric: Metric = METRIC_L2, storage: str = "fp32", device: int | None = None):
+        super().__init__(d, metric)
+        mv = metric_value(metric)
+        if mv not in ("l2", "ip"):
+            raise NotImplementedError(
+                f"metric {mv!r}: the GPU flat index implements L2 and inner product "
+                "(the reference's BLAS path, flat.py:94-118)")
+        if storage not in _STORAGE:
+            raise ValueError(f"storage must be one of fp32/fp16/bf16, got {storage!r}")
+        self.storage = storage
+        self._mcode = N.FK_METRIC_L2 if mv == "l2" else N.FK_METRIC_IP
+        if device is None:
+            device = torch.cuda.current_device() if (torch is not None and torch.cuda.is_available()) else 0
+        self.device = int(device)
+        L = N.lib()
+        h = ctypes.c_void_p()
+        N.check(L.fk_create(self.device, self.d, self._mcode, _STORAGE[storage], ctypes.byref(h)))
+        self._h = h
+        self._pos_of_id: dict[int, int] | None = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                N.lib().fk_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    # ------------------------------------------------------------------ storage
+    def _add(self, x, ids, sequential: bool) -> None:
+        """flat.py:28-32: append vectors, ids and norms (on device)."""
+        if x.shape[0] == 0:
+            return
+        dev = is_torch(x) and x.is_cuda
+        if dev and x.device.index != self.device:
+            x = x.to(f"cuda:{self.device}")
+        if not dev and is_torch(x):
+            x = x.contiguous()
+        ids_arg = None
+        keep = None
+        if not sequential:
+            if dev:
+                t = ids if is_torch(ids) else torch.from_numpy(np.ascontiguousarray(ids, dtype=np.int64))
+                keep = t.to(device=x.device, dtype=torch.int64).contiguous()
+            else:
+                keep = np.ascontiguousarray(ids.cpu().numpy() if is_torch(ids) else ids, dtype=np.int64)
+            ids_arg = _ptr(keep)
+        stream = _stream_of(self.device) if dev else 0
+        N.check(N.lib().fk_add(self._h, _ptr(x), x.shape[0], _dtype_code(x), ids_arg, int(dev), stream))
+        self._pos_of_id = None
+
+    def reset(self) -> None:
+        """Drop every vector (Faiss ``Index::reset``; not in the reference)."""
+        N.check(N.lib().fk_reset(self._h))
+        self.ntotal = 0
+        self._pos_of_id = None
+
+    @property
+    def ids(self) -> np.ndarray:
+        """Stored ids in storage order (the reference's ``FlatIndex.ids``)."""
+        out = np.empty(self.ntotal, dtype=np.int64)
+        if self.ntotal:
+            N.check(N.lib().fk_get_ids(self._h, out.ctypes.data))
+        return out
+
+    @property
+    def vectors(self) -> np.ndarray:
+        """Stored vectors as float32 (the reference's ``FlatIndex.vectors``)."""
+        pos = np.arange(self.ntotal, dtype=np.int64)
+        return self._reconstruct_positions(pos)
+
+    def _positions(self, ids) -> np.ndarray:
+        """flat.py:34-41: id -> storage position, KeyError on unknown ids."""
+        if self._pos_of_id is None:
+            self._pos_of_id = {int(v): i for i, v in enumerate(self.ids)}
+        try:
+            return np.array([self._pos_of_id[int(v)] for v in np.atleast_1d(np.asarray(ids))], dtype=np.int64)
+        except KeyError as exc:
+            raise KeyError(f"unknown id {exc.args[0]}") from None
+
+    def _reconstruct_positions(self, pos: np.ndarray) -> np.ndarray:
+        out = np.empty((len(pos), self.d), dtype=np.float32)
+        if len(pos):
+            N.check(N.lib().fk_reconstruct(self._h, np.ascontiguousarray(pos).ctypes.data, len(pos),
+                                           out.ctypes.data, 0, 0))
+        return out
+
+    def reconstruct_batch(self, ids) -> np.ndarray:
+        """flat.py:43-44 (exact: fp32 storage keeps hi+lo == x)."""
+        return self._reconstruct_positions(self._positions(ids))
+
+    def remove_ids(self, ids) -> int:
+        """flat.py:46-56: drop matching ids, keep storage order."""
+        arr = np.ascontiguousarray(np.atleast_1d(np.asarray(ids, dtype=np.int64)))
+        removed = ctypes.c_int64(0)
+        N.check(N.lib().fk_remove_ids(self._h, arr.ctypes.data, arr.size, 0, ctypes.byref(removed), 0))
+        self.ntotal -= int(removed.value)
+        if removed.value:
+            self._pos_of_id = None
+        return int(removed.value)
+
+    # ------------------------------------------------------------------ search
+    def _search(self, q, k: int, with_positions: bool = False):
+        """flat.py:58-62 / 94-118 on the GPU; returns SearchResult (+ positions)."""
+        nq = q.shape[0]
+        L = N.lib()
+        if is_torch(q) and q.is_cuda:
+            if q.device.index != self.device:
+                q = q.to(f"cuda:{self.device}")
+            dev = q.device
+            D = torch.empty((nq, k), dtype=torch.float32, device=dev)
+            I = torch.empty((nq, k), dtype=torch.int64, device=dev)
+            P = torch.empty((nq, k), dtype=torch.int64, device=dev) if with_positions else None
+            N.check(L.fk_search(self._h, _ptr(q), nq, _dtype_code(q), k, _ptr(D), _ptr(I),
+                                _ptr(P) if P is not None else None, 1, _stream_of(self.device)))
+        else:
+            if is_torch(q):
+                q = q.contiguous()
+            D = np.empty((nq, k), dtype=np.float32)
+            I = np.empty((nq, k), dtype=np.int64)
+            P = np.empty((nq, k), dtype=np.int64) if with_positions else None
+            N.check(L.fk_search(self._h, _ptr(q), nq, _dtype_code(q), k, D.ctypes.data, I.ctypes.data,
+                                P.ctypes.data if P is not None else None, 0, 0))
+        res = SearchResult(I, D, k)
+        return (res, P) if with_positions else res
+
+    def search_with_positions(self, q, k: int):
+        """Search returning (SearchResult, storage positions) -- the sharded
+        index orders cross-shard ties by global position."""
+        if k < 1:
+            raise ValueError("k must be >= 1")
+        return self._search(as_vectors(q, self.d), int(k), with_positions=True)
+
+    # ------------------------------------------------------------------ instrumentation
+    def set_profiling(self, on: bool) -> None:
+        N.check(N.lib().fk_set_profiling(self._h, int(on)))
+
+    def kernel_times(self):
+        """(prep_ms, fused_ms, merge_ms), launches of the last search."""
+        ms = (ctypes.c_float * 3)()
+        nl = ctypes.c_int(0)
+        N.check(N.lib().fk_kernel_times(self._h, ms, ctypes.byref(nl)))
+        return (ms[0], ms[1], ms[2]), nl.value
+
+    def last_plan(self) -> dict:
+        v = (ctypes.c_int * 8)()
+        N.check(N.lib().fk_last_plan(self._h, v))
+        keys = ("grid", "S", "chunk_tiles", "units", "stages", "a_resident", "smem", "kq")
+        return dict(zip(keys, list(v)))
+
+
+class IndexFlatL2(FlatIndex):
+    """Faiss-style alias: ``IndexFlatL2(d)``."""
+
+    def __init__(self, d: int, storage: str = "fp32", device: int | None = None):
+        super().__init__(d, METRIC_L2, storage=storage, device=device)
+
+
+class IndexFlatIP(FlatIndex):
+    """Faiss-style alias: ``IndexFlatIP(d)``."""
+
+    def __init__(self, d: int, storage: str = "fp32", device: int | None = None):
+        super().__init__(d, METRIC_IP, storage=storage, device=device)
