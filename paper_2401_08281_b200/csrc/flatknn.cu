@@ -89,7 +89,7 @@ int make_map(CUtensorMap* m, const void* base, int elem_bytes, uint64_t cols, ui
 }
 
 constexpr int SMEM_LIMIT = 232448;  // sm_100 max dynamic smem per block (227 KB)
-constexpr int SMEM_RESERVE = 1024 /*align*/ + 256 /*barriers + tmem slot*/;
+constexpr int SMEM_RESERVE = 1024 /*align*/ + 2 * BN * 4 /*norm tiles*/ + 256 /*barriers + tmem slot*/;
 
 int elem_bytes_of(int storage) { return storage == FK_F32 ? 4 : 2; }
 int chunk_elems_of(int storage) { return storage == FK_F32 ? 32 : 64; }
@@ -211,41 +211,50 @@ int launch_prep(int storage, const void* x, int dtype, int64_t n, int d, int dp,
 
 size_t dtype_bytes(int dtype) { return dtype == FK_F32 ? 4 : 2; }
 
-template <int MODE, int KQ, bool IP>
+template <int MODE, int KQ, bool IP, int EPI>
 int launch_fused_t(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0, const CUtensorMap& b1,
                    const SearchParams& sp, int grid, int smem, cudaStream_t st) {
-  auto kern = fused_knn_kernel<MODE, KQ, IP>;
-  static int configured_smem = 0;  // per instantiation
-  if (configured_smem < smem) {
+  auto kern = fused_knn_kernel<MODE, KQ, IP, EPI>;
+  static bool configured = false;  // per instantiation
+  if (!configured) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
-    configured_smem = SMEM_LIMIT;
+    configured = true;
   }
-  kern<<<grid, NUM_THREADS, smem, st>>>(a0, a1, b0, b1, sp);
+  kern<<<grid, 128 + 32 * EPI, smem, st>>>(a0, a1, b0, b1, sp);
   CKL();
   return FK_OK;
 }
 
-template <int MODE, bool IP>
+template <int MODE, bool IP, int EPI>
 int launch_fused_k(int kq, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
                    const CUtensorMap& b1, const SearchParams& sp, int grid, int smem, cudaStream_t st) {
   switch (kq) {
-    case 8: return launch_fused_t<MODE, 8, IP>(a0, a1, b0, b1, sp, grid, smem, st);
-    case 16: return launch_fused_t<MODE, 16, IP>(a0, a1, b0, b1, sp, grid, smem, st);
-    case 32: return launch_fused_t<MODE, 32, IP>(a0, a1, b0, b1, sp, grid, smem, st);
+    case 8: return launch_fused_t<MODE, 8, IP, EPI>(a0, a1, b0, b1, sp, grid, smem, st);
+    case 16: return launch_fused_t<MODE, 16, IP, EPI>(a0, a1, b0, b1, sp, grid, smem, st);
+    case 32: return launch_fused_t<MODE, 32, IP, EPI>(a0, a1, b0, b1, sp, grid, smem, st);
   }
   return set_err(FK_E_UNSUPPORTED, "queue bucket %d", kq);
 }
 
-int launch_fused(int storage, bool ip, int kq, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
-                 const CUtensorMap& b1, const SearchParams& sp, int grid, int smem, cudaStream_t st) {
+template <int EPI>
+int launch_fused_e(int storage, bool ip, int kq, const CUtensorMap& a0, const CUtensorMap& a1,
+                   const CUtensorMap& b0, const CUtensorMap& b1, const SearchParams& sp, int grid, int smem,
+                   cudaStream_t st) {
   if (storage == FK_F32)
-    return ip ? launch_fused_k<0, true>(kq, a0, a1, b0, b1, sp, grid, smem, st)
-              : launch_fused_k<0, false>(kq, a0, a1, b0, b1, sp, grid, smem, st);
+    return ip ? launch_fused_k<0, true, EPI>(kq, a0, a1, b0, b1, sp, grid, smem, st)
+              : launch_fused_k<0, false, EPI>(kq, a0, a1, b0, b1, sp, grid, smem, st);
   if (storage == FK_F16)
-    return ip ? launch_fused_k<1, true>(kq, a0, a1, b0, b1, sp, grid, smem, st)
-              : launch_fused_k<1, false>(kq, a0, a1, b0, b1, sp, grid, smem, st);
-  return ip ? launch_fused_k<2, true>(kq, a0, a1, b0, b1, sp, grid, smem, st)
-            : launch_fused_k<2, false>(kq, a0, a1, b0, b1, sp, grid, smem, st);
+    return ip ? launch_fused_k<1, true, EPI>(kq, a0, a1, b0, b1, sp, grid, smem, st)
+              : launch_fused_k<1, false, EPI>(kq, a0, a1, b0, b1, sp, grid, smem, st);
+  return ip ? launch_fused_k<2, true, EPI>(kq, a0, a1, b0, b1, sp, grid, smem, st)
+            : launch_fused_k<2, false, EPI>(kq, a0, a1, b0, b1, sp, grid, smem, st);
+}
+
+int launch_fused(int epi, int storage, bool ip, int kq, const CUtensorMap& a0, const CUtensorMap& a1,
+                 const CUtensorMap& b0, const CUtensorMap& b1, const SearchParams& sp, int grid, int smem,
+                 cudaStream_t st) {
+  if (epi == 8) return launch_fused_e<8>(storage, ip, kq, a0, a1, b0, b1, sp, grid, smem, st);
+  return launch_fused_e<4>(storage, ip, kq, a0, a1, b0, b1, sp, grid, smem, st);
 }
 
 // Split-N plan: choose the number of N-chunks S so that num_m*S work units
@@ -253,11 +262,11 @@ int launch_fused(int storage, bool ip, int kq, const CUtensorMap& a0, const CUte
 // one contiguous range of base tiles).  Units are ordered chunk-major, so the
 // CTAs resident at any moment stream the same ~2 chunks of the base through
 // L2 (the base is read from HBM about once per wave).
-void plan_split(int num_m, int n_tiles, int num_sms, int* S_out, int* chunk_out) {
+void plan_split(int num_m, int n_tiles, int num_sms, int max_S, int* S_out, int* chunk_out) {
   double best_cost = 1e300;
   int bestS = 1, bestC = n_tiles;
   const double ovh = 1.5;  // per-unit cost in tile-equivalents (A reload, pipeline fill, flush)
-  const int smax = std::min(128, n_tiles);
+  const int smax = std::min(max_S, n_tiles);
   for (int S = 1; S <= smax; ++S) {
     const int chunk = (n_tiles + S - 1) / S;
     const int s_eff = (n_tiles + chunk - 1) / chunk;
@@ -444,12 +453,15 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
     h->nlaunch++;
 
     // ---- plan
+    int epi = 4;
+    if (const char* e = getenv("FK_EPI")) epi = atoi(e) == 8 ? 8 : 4;
+    const int nh = epi / 4;
     const int num_m = (int)((nq + BM - 1) / BM);
     const int n_tiles = (int)((h->ntotal + BN - 1) / BN);
     int S, chunk_tiles;
-    plan_split(num_m, n_tiles, h->num_sms, &S, &chunk_tiles);
+    plan_split(num_m, n_tiles, h->num_sms, 128 / nh, &S, &chunk_tiles);
     if (const char* e = getenv("FK_FORCE_S")) {
-      S = std::max(1, std::min(atoi(e), std::min(128, n_tiles)));
+      S = std::max(1, std::min(atoi(e), std::min(128 / nh, n_tiles)));
       chunk_tiles = (n_tiles + S - 1) / S;
       S = (n_tiles + chunk_tiles - 1) / chunk_tiles;
     }
@@ -458,24 +470,27 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
     const int split = split_of(h->storage);
     const int num_kb = h->dp / chunk_elems_of(h->storage);
     const int a_bytes = split * num_kb * (int)CHUNK_BYTES;
-    int a_res = 1;
-    int stages = (SMEM_LIMIT - SMEM_RESERVE - a_bytes) / (split * (int)CHUNK_BYTES);
-    if (stages < 3) {
-      a_res = 0;
-      stages = (SMEM_LIMIT - SMEM_RESERVE) / (2 * split * (int)CHUNK_BYTES);
+    const int a_tmem_cols = h->storage == FK_F32 ? 2 * h->dp : h->dp / 2;
+    int a_mode = a_tmem_cols <= 256 ? 0 : 1;
+    if (const char* e = getenv("FK_FORCE_AMODE")) a_mode = std::max(0, std::min(2, atoi(e)));
+    if (a_mode == 0 && a_tmem_cols > 256) a_mode = 1;
+    auto stages_for = [&](int mode) {
+      const int avail = SMEM_LIMIT - SMEM_RESERVE - (mode == 1 ? a_bytes : 0);
+      return avail / ((mode == 2 ? 2 : 1) * split * (int)CHUNK_BYTES);
+    };
+    int stages = stages_for(a_mode);
+    if (a_mode == 1 && stages < 3) {
+      a_mode = 2;
+      stages = stages_for(2);
     }
     stages = std::min(stages, 8);
+    if (const char* e = getenv("FK_STAGES")) stages = std::max(2, std::min(stages, atoi(e)));
     if (stages < 2) return set_err(FK_E_UNSUPPORTED, "pipeline does not fit in shared memory");
-    if (const char* e = getenv("FK_FORCE_STREAM_A")) {
-      if (atoi(e)) {
-        a_res = 0;
-        stages = std::min(8, (SMEM_LIMIT - SMEM_RESERVE) / (2 * split * (int)CHUNK_BYTES));
-      }
-    }
-    const int smem = SMEM_RESERVE + (a_res ? a_bytes : 0) + stages * (a_res ? 1 : 2) * split * (int)CHUNK_BYTES;
+    const int smem = SMEM_RESERVE + (a_mode == 1 ? a_bytes : 0) + stages * (a_mode == 2 ? 2 : 1) * split * (int)CHUNK_BYTES;
+    const int S_tot = S * nh;
 
-    if ((rc = h->pkey.ensure((size_t)nq * S * k * sizeof(uint32_t)))) return rc;
-    if ((rc = h->ppos.ensure((size_t)nq * S * k * sizeof(uint32_t)))) return rc;
+    if ((rc = h->pkey.ensure((size_t)nq * S_tot * k * sizeof(uint32_t)))) return rc;
+    if ((rc = h->ppos.ensure((size_t)nq * S_tot * k * sizeof(uint32_t)))) return rc;
 
     CUtensorMap ta0, ta1, tb0, tb1;
     const int eb = elem_bytes_of(h->storage);
@@ -503,28 +518,30 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
     sp.S = S;
     sp.num_units = num_units;
     sp.num_kb = num_kb;
-    sp.a_resident = a_res;
+    sp.a_mode = a_mode;
+    sp.qa0 = h->q0.p;
+    sp.qa1 = h->q1.p;
     sp.stages = stages;
     h->plan[0] = grid;
     h->plan[1] = S;
     h->plan[2] = chunk_tiles;
     h->plan[3] = num_units;
     h->plan[4] = stages;
-    h->plan[5] = a_res;
+    h->plan[5] = a_mode;
     h->plan[6] = smem;
-    h->plan[7] = kq;
+    h->plan[7] = kq * 100 + epi;
 
     if (ev) CK(cudaEventRecord(ev[1], st));
-    if ((rc = launch_fused(h->storage, ip, kq, ta0, ta1, tb0, tb1, sp, grid, smem, st))) return rc;
+    if ((rc = launch_fused(epi, h->storage, ip, kq, ta0, ta1, tb0, tb1, sp, grid, smem, st))) return rc;
     h->nlaunch++;
     if (ev) CK(cudaEventRecord(ev[2], st));
 
     const int wpb = 8;
     const unsigned mgrid = (unsigned)((nq + wpb - 1) / wpb);
     if (ip)
-      merge_kernel<true><<<mgrid, wpb * 32, 0, st>>>(sp.part_key, sp.part_pos, S, (int)nq, k, h->ids, dD, dI, dP);
+      merge_kernel<true><<<mgrid, wpb * 32, 0, st>>>(sp.part_key, sp.part_pos, S_tot, (int)nq, k, h->ids, dD, dI, dP);
     else
-      merge_kernel<false><<<mgrid, wpb * 32, 0, st>>>(sp.part_key, sp.part_pos, S, (int)nq, k, h->ids, dD, dI, dP);
+      merge_kernel<false><<<mgrid, wpb * 32, 0, st>>>(sp.part_key, sp.part_pos, S_tot, (int)nq, k, h->ids, dD, dI, dP);
     CKL();
     h->nlaunch++;
     if (ev) CK(cudaEventRecord(ev[3], st));

@@ -24,9 +24,7 @@ namespace fk {
 constexpr int BM = 128;                        // queries per tile (TMEM lanes)
 constexpr int BN = 128;                        // base rows per tile (TMEM columns)
 constexpr uint32_t CHUNK_BYTES = 128u * 128u;  // one 128-row x 128-byte K-chunk
-constexpr int TMEM_COLS = 2 * BN;              // double-buffered accumulator
-constexpr int NUM_THREADS = 256;               // 4 control warps + 4 epilogue warps
-constexpr int EPI_WARP0 = 4;
+constexpr int EPI_WARP0 = 4;                   // warps 0-3: producer, MMA, TMEM alloc, spare
 
 // ------------------------------------------------------------ key helpers
 // Order-preserving float32 -> uint32 (core.py:193-197): NaN above +inf,
@@ -47,10 +45,12 @@ struct SearchParams {
   uint32_t* part_key;  // [nq][S][k]
   uint32_t* part_pos;  // [nq][S][k]
   float* dbg_ip;       // optional raw inner products [nq][nb] (debug)
+  const void* qa0;     // query operand rows [nq][dp] (hi / f16 / bf16) -- A_TMEM mode
+  const void* qa1;     // lo part (fp32 mode)
   int nq, nb, k;
   int num_m, n_tiles, chunk_tiles, S, num_units;
   int num_kb;      // padded d / elements-per-128B-chunk
-  int a_resident;  // queries kept in smem for a whole work unit
+  int a_mode;      // 0: queries in TMEM, 1: resident in smem, 2: streamed per stage
   int stages;      // B (and streamed A) pipeline depth
 };
 
@@ -82,10 +82,39 @@ __device__ __forceinline__ void queue_insert(uint32_t (&keys)[KQ], uint32_t (&po
 }
 
 // ------------------------------------------------------------ fused kernel
-// MODE 0: fp32 storage, 3xTF32 (A_hi.B_hi + A_hi.B_lo + A_lo.B_hi)
-// MODE 1: fp16, MODE 2: bf16 (single kind::f16 pass)
-template <int MODE, int KQ, bool IS_IP>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+// Work unit = (128-query tile m, N-chunk): the CTA keeps the queries of tile m
+// resident (TMEM or smem) and streams the chunk's base tiles through a TMA ring.
+//
+// Warp roles (1 CTA per SM, persistent):
+//   warp 0      TMA producer (one lane): B tiles (and A when not resident)
+//   warp 1      MMA issuer (one lane): tcgen05.mma into a double-buffered
+//               TMEM accumulator; also bulk-copies the tile's base norms
+//   warp 2      TMEM allocator
+//   warps 4..   EPI epilogue warps: write the query tile into TMEM (A_TMEM
+//               mode), then per accumulator tile: tcgen05.ld -> distance
+//               -> NaN-propagating min-tree filter -> rare exact insertion
+//               into a per-row register queue.
+//
+// a_mode 0: queries in TMEM (TS MMA; frees smem, halves smem operand reads)
+// a_mode 1: queries resident in smem for the unit
+// a_mode 2: queries streamed with every B stage (large d)
+constexpr int TMEM_A_COL = 2 * BN;  // A operand columns start after the accumulators
+
+__device__ __forceinline__ float select32(const float (&s)[32], int j) {
+  float t16[16], t8[8], t4[4], t2[2];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) t16[i] = (j & 1) ? s[2 * i + 1] : s[2 * i];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) t8[i] = (j & 2) ? t16[2 * i + 1] : t16[2 * i];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) t4[i] = (j & 4) ? t8[2 * i + 1] : t8[2 * i];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) t2[i] = (j & 8) ? t4[2 * i + 1] : t4[2 * i];
+  return (j & 16) ? t2[1] : t2[0];
+}
+
+template <int MODE, int KQ, bool IS_IP, int EPI>
+__global__ void __launch_bounds__(128 + 32 * EPI, 1)
     fused_knn_kernel(const __grid_constant__ CUtensorMap tm_a0, const __grid_constant__ CUtensorMap tm_a1,
                      const __grid_constant__ CUtensorMap tm_b0, const __grid_constant__ CUtensorMap tm_b1,
                      const SearchParams p) {
@@ -93,6 +122,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   constexpr int BK = (MODE == 0) ? 32 : 64;  // elements per 128-byte K-chunk
   constexpr uint32_t AB_FMT = (MODE == 0) ? 2u : (MODE == 1 ? 0u : 1u);
   constexpr uint32_t IDESC = make_idesc(AB_FMT, BM, BN);
+  constexpr int NH = EPI / 4;       // epilogue warps per TMEM lane quarter
+  constexpr int COLS = BN / NH;     // accumulator columns per epilogue warp
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -101,27 +132,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int lane = threadIdx.x & 31;
   const int num_kb = p.num_kb;
   const int stages = p.stages;
-  const bool a_res = p.a_resident != 0;
-  const uint32_t a_bytes = a_res ? SPLIT * num_kb * CHUNK_BYTES : 0u;
-  const uint32_t stage_bytes = (a_res ? SPLIT : 2 * SPLIT) * CHUNK_BYTES;
+  const int a_mode = p.a_mode;
+  const uint32_t a_bytes = (a_mode == 1) ? SPLIT * num_kb * CHUNK_BYTES : 0u;
+  const uint32_t stage_bytes = (a_mode == 2 ? 2 * SPLIT : SPLIT) * CHUNK_BYTES;
+  const uint32_t tmem_cols = (a_mode == 0) ? 512u : 256u;
 
   uint8_t* a_region = smem;
   uint8_t* st_region = smem + a_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(st_region + stages * stage_bytes);
+  float* xn_s = reinterpret_cast<float*>(st_region + stages * stage_bytes);  // [2][BN]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(xn_s + 2 * BN);
   uint64_t* full = bars;
   uint64_t* empty = bars + stages;
   uint64_t* tfull = bars + 2 * stages;
   uint64_t* tempty = tfull + 2;
-  uint64_t* afull = tempty + 2;
+  uint64_t* xfull = tempty + 2;
+  uint64_t* afull = xfull + 2;
   uint64_t* aempty = afull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 1);
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tm_a0);
     tma_prefetch_desc(&tm_b0);
-    if (SPLIT == 2) {
-      tma_prefetch_desc(&tm_a1);
-      tma_prefetch_desc(&tm_b1);
+    if (SPLIT == 2) tma_prefetch_desc(&tm_b1);
+    if (a_mode != 0) {
+      tma_prefetch_desc(&tm_a0);
+      if (SPLIT == 2) tma_prefetch_desc(&tm_a1);
     }
   }
   if (warp == 1 && lane == 0) {
@@ -131,13 +165,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);  // one arrival per epilogue warp
+      mbar_init(&tempty[b], EPI);
+      mbar_init(&xfull[b], 1);
     }
-    mbar_init(afull, 1);
+    mbar_init(afull, a_mode == 0 ? EPI : 1);
     mbar_init(aempty, 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, TMEM_COLS);
+  if (warp == 2) tmem_alloc(tmem_slot, tmem_cols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -155,7 +190,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int m = u - chunk * p.num_m;
         const int t0 = chunk * p.chunk_tiles;
         const int t1 = min(t0 + p.chunk_tiles, p.n_tiles);
-        if (a_res) {
+        if (a_mode == 1) {
           if (j > 0) mbar_wait(aempty, (j - 1) & 1);
           mbar_arrive_expect_tx(afull, a_bytes);
           for (int part = 0; part < SPLIT; ++part)
@@ -168,12 +203,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_arrive_expect_tx(&full[stage], stage_bytes);
             uint8_t* sb = st_region + stage * stage_bytes;
-            for (int part = 0; part < SPLIT; ++part)
-              tma_load_2d(sb + part * CHUNK_BYTES, part ? &tm_b1 : &tm_b0, &full[stage], kb * BK, t * BN, pol_b);
-            if (!a_res)
-              for (int part = 0; part < SPLIT; ++part)
-                tma_load_2d(sb + (SPLIT + part) * CHUNK_BYTES, part ? &tm_a1 : &tm_a0, &full[stage], kb * BK,
-                            m * BM, pol_a);
+            tma_load_2d(sb, &tm_b0, &full[stage], kb * BK, t * BN, pol_b);
+            if (SPLIT == 2) tma_load_2d(sb + CHUNK_BYTES, &tm_b1, &full[stage], kb * BK, t * BN, pol_b);
+            if (a_mode == 2) {
+              tma_load_2d(sb + SPLIT * CHUNK_BYTES, &tm_a0, &full[stage], kb * BK, m * BM, pol_a);
+              if (SPLIT == 2)
+                tma_load_2d(sb + 3 * CHUNK_BYTES, &tm_a1, &full[stage], kb * BK, m * BM, pol_a);
+            }
             if (++stage == (uint32_t)stages) {
               stage = 0;
               phase ^= 1;
@@ -187,11 +223,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       uint32_t stage = 0, phase = 0, tcount = 0;
       int j = 0;
+      const uint32_t a_tm = tmem_base + TMEM_A_COL;
+      const uint32_t a_lo_off = (MODE == 0) ? (uint32_t)(num_kb * 32) : 0u;  // lo half after hi (columns)
       for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++j) {
         const int chunk = u / p.num_m;
         const int t0 = chunk * p.chunk_tiles;
         const int t1 = min(t0 + p.chunk_tiles, p.n_tiles);
-        if (a_res) {
+        if (a_mode != 2) {
           mbar_wait(afull, j & 1);
           tc_fence_after();
         }
@@ -199,30 +237,49 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t buf = tcount & 1, tph = (tcount >> 1) & 1;
           mbar_wait(&tempty[buf], tph ^ 1);
           tc_fence_after();
+          if (!IS_IP) {
+            mbar_arrive_expect_tx(&xfull[buf], BN * sizeof(float));
+            bulk_load(xn_s + buf * BN, p.xnorm + (size_t)t * BN, BN * sizeof(float), &xfull[buf]);
+          }
           const uint32_t d_tmem = tmem_base + buf * BN;
           for (int kb = 0; kb < num_kb; ++kb) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
             uint8_t* sb = st_region + stage * stage_bytes;
-            const uint8_t* a0 = a_res ? a_region + kb * CHUNK_BYTES : sb + SPLIT * CHUNK_BYTES;
-            const uint64_t ad0 = smem_desc_sw128(smem_u32(a0));
             const uint64_t bd0 = smem_desc_sw128(smem_u32(sb));
-            if (MODE == 0) {
-              const uint8_t* a1 = a_res ? a_region + (num_kb + kb) * CHUNK_BYTES : sb + 3 * CHUNK_BYTES;
-              const uint64_t ad1 = smem_desc_sw128(smem_u32(a1));
-              const uint64_t bd1 = smem_desc_sw128(smem_u32(sb + CHUNK_BYTES));
+            if (a_mode == 0) {
+              const uint32_t ah = a_tm + kb * 32;
+              if (MODE == 0) {
+                const uint64_t bd1 = smem_desc_sw128(smem_u32(sb + CHUNK_BYTES));
 #pragma unroll
-              for (int kk = 0; kk < 4; ++kk) {
-                const uint64_t off = 2 * kk;  // 32 bytes per K=8 tf32 step, in 16-byte units
-                mma_tf32(d_tmem, ad1 + off, bd0 + off, IDESC, (kb | kk) != 0);  // lo * hi
-                mma_tf32(d_tmem, ad0 + off, bd1 + off, IDESC, 1u);              // hi * lo
-                mma_tf32(d_tmem, ad0 + off, bd0 + off, IDESC, 1u);              // hi * hi
+                for (int kk = 0; kk < 4; ++kk) {
+                  const uint64_t off = 2 * kk;  // 32 B = K 8 (tf32) per step, 16-byte units
+                  mma_tf32_ts(d_tmem, ah + a_lo_off + 8 * kk, bd0 + off, IDESC, (kb | kk) != 0);  // lo*hi
+                  mma_tf32_ts(d_tmem, ah + 8 * kk, bd1 + off, IDESC, 1u);                        // hi*lo
+                  mma_tf32_ts(d_tmem, ah + 8 * kk, bd0 + off, IDESC, 1u);                        // hi*hi
+                }
+              } else {
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                  mma_f16_ts(d_tmem, ah + 8 * kk, bd0 + 2 * kk, IDESC, (kb | kk) != 0);
               }
             } else {
+              const uint8_t* a0 = (a_mode == 1) ? a_region + kb * CHUNK_BYTES : sb + SPLIT * CHUNK_BYTES;
+              const uint64_t ad0 = smem_desc_sw128(smem_u32(a0));
+              if (MODE == 0) {
+                const uint8_t* a1 = (a_mode == 1) ? a_region + (num_kb + kb) * CHUNK_BYTES : sb + 3 * CHUNK_BYTES;
+                const uint64_t ad1 = smem_desc_sw128(smem_u32(a1));
+                const uint64_t bd1 = smem_desc_sw128(smem_u32(sb + CHUNK_BYTES));
 #pragma unroll
-              for (int kk = 0; kk < 4; ++kk) {
-                const uint64_t off = 2 * kk;  // 32 bytes per K=16 f16 step
-                mma_f16(d_tmem, ad0 + off, bd0 + off, IDESC, (kb | kk) != 0);
+                for (int kk = 0; kk < 4; ++kk) {
+                  const uint64_t off = 2 * kk;
+                  mma_tf32(d_tmem, ad1 + off, bd0 + off, IDESC, (kb | kk) != 0);
+                  mma_tf32(d_tmem, ad0 + off, bd1 + off, IDESC, 1u);
+                  mma_tf32(d_tmem, ad0 + off, bd0 + off, IDESC, 1u);
+                }
+              } else {
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) mma_f16(d_tmem, ad0 + 2 * kk, bd0 + 2 * kk, IDESC, (kb | kk) != 0);
               }
             }
             mma_commit(&empty[stage]);
@@ -233,14 +290,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           mma_commit(&tfull[buf]);
         }
-        if (a_res) mma_commit(aempty);
+        if (a_mode == 1) mma_commit(aempty);
       }
     }
   } else if (warp >= EPI_WARP0) {
-    // ===================== epilogue: TMEM -> distances -> top-k =====================
+    // ===================== epilogue =====================
+    const int ew = warp - EPI_WARP0;
     const int eq = warp & 3;  // TMEM lane quarter this warp may access
+    const int h = ew >> 2;    // column slice of the accumulator
     const uint32_t lane_addr = static_cast<uint32_t>(eq * 32) << 16;
     const int k = p.k;
+    const int dp = num_kb * BK;
+    const int a_cols = (MODE == 0) ? 2 * dp : dp / 2;  // TMEM columns of the query operand
     uint32_t tcount = 0;
     for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
       const int chunk = u / p.num_m;
@@ -249,8 +310,36 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int t1 = min(t0 + p.chunk_tiles, p.n_tiles);
       const int row = m * BM + eq * 32 + lane;
       const bool row_ok = row < p.nq;
-      const float qn = (!IS_IP && row_ok) ? p.qnorm[row] : 0.f;
 
+      if (a_mode == 0) {
+        // Query tile -> TMEM (lane = query row, columns = K; fp32: [hi | lo]).
+        // Safe: every MMA of the previous unit retired before its last tfull.
+        for (int cc = h; cc < a_cols / 32; cc += NH) {
+          uint32_t v[32];
+          const uint32_t* src;
+          if (MODE == 0)
+            src = (cc * 32 < dp) ? reinterpret_cast<const uint32_t*>(p.qa0) + (size_t)row * dp + cc * 32
+                                 : reinterpret_cast<const uint32_t*>(p.qa1) + (size_t)row * dp + (cc * 32 - dp);
+          else
+            src = reinterpret_cast<const uint32_t*>(p.qa0) + (size_t)row * (dp / 2) + cc * 32;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            uint4 w = make_uint4(0u, 0u, 0u, 0u);
+            if (row_ok) w = __ldg(reinterpret_cast<const uint4*>(src) + i);
+            v[4 * i] = w.x;
+            v[4 * i + 1] = w.y;
+            v[4 * i + 2] = w.z;
+            v[4 * i + 3] = w.w;
+          }
+          tmem_st_32x32b_x32(tmem_base + lane_addr + TMEM_A_COL + cc * 32, v);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(afull);
+      }
+
+      const float qn = (!IS_IP && row_ok) ? p.qnorm[row] : 0.f;
       uint32_t keys[KQ], pos[KQ];
 #pragma unroll
       for (int i = 0; i < KQ; ++i) {
@@ -262,43 +351,58 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int t = t0; t < t1; ++t, ++tcount) {
         const uint32_t buf = tcount & 1, tph = (tcount >> 1) & 1;
         mbar_wait(&tfull[buf], tph);
+        if (!IS_IP) mbar_wait(&xfull[buf], tph);
         tc_fence_after();
-        const int n0 = t * BN;
+        const int n0 = t * BN + h * COLS;
         const int nvalid = p.nb - n0;
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = 0; c < COLS / 32; ++c) {
           uint32_t r[32];
-          tmem_ld_32x32b_x32(tmem_base + lane_addr + buf * BN + c * 32, r);
+          tmem_ld_32x32b_x32(tmem_base + lane_addr + buf * BN + h * COLS + c * 32, r);
           tmem_ld_wait();
           if (p.dbg_ip != nullptr && row_ok) {
             for (int j = 0; j < 32; ++j)
-              if (c * 32 + j < nvalid)
-                p.dbg_ip[(size_t)row * p.nb + n0 + c * 32 + j] = __uint_as_float(r[j]);
+              if (c * 32 + j < nvalid) p.dbg_ip[(size_t)row * p.nb + n0 + c * 32 + j] = __uint_as_float(r[j]);
           }
-          const float4* xn4 = reinterpret_cast<const float4*>(p.xnorm + n0 + c * 32);
+          float s[32];
+          if (IS_IP) {
 #pragma unroll
-          for (int j4 = 0; j4 < 8; ++j4) {
-            float xs[4] = {0.f, 0.f, 0.f, 0.f};
-            if (!IS_IP) {
-              const float4 v = __ldg(xn4 + j4);
-              xs[0] = v.x;
-              xs[1] = v.y;
-              xs[2] = v.z;
-              xs[3] = v.w;
+            for (int j = 0; j < 32; ++j) s[j] = -__uint_as_float(r[j]);
+          } else {
+            const float4* xs4 = reinterpret_cast<const float4*>(xn_s + buf * BN + h * COLS + c * 32);
+#pragma unroll
+            for (int j4 = 0; j4 < 8; ++j4) {
+              const float4 x = xs4[j4];
+              // flat.py:111: (qn + norms) - 2.0*ip ; 2*ip is exact -> one FMA
+              s[4 * j4 + 0] = fmaf(-2.f, __uint_as_float(r[4 * j4 + 0]), qn + x.x);
+              s[4 * j4 + 1] = fmaf(-2.f, __uint_as_float(r[4 * j4 + 1]), qn + x.y);
+              s[4 * j4 + 2] = fmaf(-2.f, __uint_as_float(r[4 * j4 + 2]), qn + x.z);
+              s[4 * j4 + 3] = fmaf(-2.f, __uint_as_float(r[4 * j4 + 3]), qn + x.w);
             }
+          }
+          float mn[16];
 #pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {
-              const int j = j4 * 4 + jj;
-              const float ip = __uint_as_float(r[j]);
-              // flat.py:111: dmat = (qn + norms) - 2.0*ip  (2*ip exact -> one FMA)
-              float s = IS_IP ? -ip : fmaf(-2.f, ip, qn + xs[jj]);
-              if (!(s > thr)) {
-                const int col = c * 32 + j;
-                if (col < nvalid) {
-                  if (!IS_IP) s = (s <= 0.f) ? 0.f : s;  // np.maximum(dmat, 0) (flat.py:112)
-                  queue_insert<KQ>(keys, pos, monotone(s), static_cast<uint32_t>(n0 + col));
-                  thr = unmonotone(keys[KQ - 1]);
-                }
+          for (int i = 0; i < 16; ++i) mn[i] = fmin_nan(s[2 * i], s[2 * i + 1]);
+#pragma unroll
+          for (int w = 8; w > 0; w >>= 1)
+#pragma unroll
+            for (int i = 0; i < w; ++i) mn[i] = fmin_nan(mn[i], mn[i + w]);
+          if (!(mn[0] > thr)) {
+            // rare path: exact (value, position) insertion of every survivor
+            const int lim = nvalid - c * 32;
+            uint32_t mask = lim >= 32 ? 0xFFFFFFFFu : (lim <= 0 ? 0u : ((1u << lim) - 1u));
+            uint32_t cand = 0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) cand |= (!(s[j] > thr) ? 1u : 0u) << j;
+            cand &= mask;
+            while (cand) {
+              const int j = __ffs(cand) - 1;
+              cand &= cand - 1;
+              float v = select32(s, j);
+              if (!(v > thr)) {
+                if (!IS_IP) v = (v <= 0.f) ? 0.f : v;  // np.maximum(dmat, 0) (flat.py:112)
+                queue_insert<KQ>(keys, pos, monotone(v), static_cast<uint32_t>(n0 + c * 32 + j));
+                thr = unmonotone(keys[KQ - 1]);
               }
             }
           }
@@ -308,7 +412,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (lane == 0) mbar_arrive(&tempty[buf]);
       }
       if (row_ok) {
-        const size_t base = ((size_t)row * p.S + chunk) * (size_t)k;
+        const int S_tot = p.S * NH;
+        const size_t base = ((size_t)row * S_tot + chunk * NH + h) * (size_t)k;
 #pragma unroll
         for (int i = 0; i < KQ; ++i) {
           if (i >= KQ - k) {
@@ -324,7 +429,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, TMEM_COLS);
+    tmem_dealloc(tmem_base, tmem_cols);
   }
 }
 

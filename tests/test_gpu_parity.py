@@ -196,13 +196,17 @@ def test_tensor_core_inner_products_vs_fp64():
         assert err < tol, (storage, err)
 
 
-@pytest.mark.parametrize("force", [("FK_FORCE_S", "1"), ("FK_FORCE_S", "7"), ("FK_FORCE_S", "64"),
-                                   ("FK_FORCE_STREAM_A", "1")])
-def test_plan_invariance(force):
+PLAN_VARIANTS = [("FK_FORCE_S", "1"), ("FK_FORCE_S", "7"), ("FK_FORCE_S", "64"), ("FK_FORCE_AMODE", "1"),
+                 ("FK_FORCE_AMODE", "2"), ("FK_EPI", "8"), ("FK_STAGES", "2")]
+
+
+@pytest.mark.parametrize("storage", ["fp32", "bf16"])
+@pytest.mark.parametrize("force", PLAN_VARIANTS)
+def test_plan_invariance(force, storage):
     rng = np.random.default_rng(6)
     xb = rng.standard_normal((20000, 100), dtype=np.float32)
     q = rng.standard_normal((333, 100), dtype=np.float32)
-    idx = IndexFlatL2(100)
+    idx = FlatIndex(100, METRIC_L2, storage=storage)
     idx.add(xb)
     base = idx.search(q, 10)
     os.environ[force[0]] = force[1]
