@@ -125,8 +125,9 @@ struct fk_index {
   void* s0 = nullptr;        // stored operand (hi / f16 / bf16) [cap][dp]
   void* s1 = nullptr;        // lo part (fp32 mode) [cap][dp]
   float* norms = nullptr;    // [cap]
+  float* xn_max = nullptr;   // device scalar: max stored norm
   int64_t* ids = nullptr;    // [cap]
-  DevBuf q_in, q0, q1, qn, pkey, ppos, outD, outI, outP, stage_in, stage_ids;
+  DevBuf q_in, q0, q1, qn, pkey, ppos, thr, outD, outI, outP, stage_in, stage_ids;
   std::mutex mu;
   int num_sms = 148;
   int profiling = 0;
@@ -317,6 +318,10 @@ int fk_create(int device, int d, int metric, int storage, fk_index** out) {
   h->metric = metric;
   h->storage = storage;
   h->num_sms = prop.multiProcessorCount;
+  if (cudaMalloc((void**)&h->xn_max, sizeof(float)) != cudaSuccess || cudaMemset(h->xn_max, 0, sizeof(float)) != cudaSuccess) {
+    delete h;
+    return set_err(FK_E_NOMEM, "cudaMalloc failed");
+  }
   if (const char* e = getenv("FK_NUM_SMS")) h->num_sms = std::max(1, std::min(atoi(e), h->num_sms));
   *out = h;
   return FK_OK;
@@ -330,9 +335,10 @@ void fk_destroy(fk_index* h) {
   cudaFree(h->s1);
   cudaFree(h->norms);
   cudaFree(h->ids);
-  for (DevBuf* b : {&h->q_in, &h->q0, &h->q1, &h->qn, &h->pkey, &h->ppos, &h->outD, &h->outI, &h->outP,
+  for (DevBuf* b : {&h->q_in, &h->q0, &h->q1, &h->qn, &h->pkey, &h->ppos, &h->thr, &h->outD, &h->outI, &h->outP,
                     &h->stage_in, &h->stage_ids})
     b->release();
+  cudaFree(h->xn_max);
   for (auto& q : h->ev_pool)
     for (auto& e : q) cudaEventDestroy(e);
   delete h;
@@ -344,6 +350,8 @@ int fk_dim(const fk_index* h) { return h ? h->d : -1; }
 int fk_reset(fk_index* h) {
   if (!h) return set_err(FK_E_INVALID, "NULL index");
   std::lock_guard<std::mutex> g(h->mu);
+  CK(cudaSetDevice(h->device));
+  CK(cudaMemset(h->xn_max, 0, sizeof(float)));
   h->ntotal = 0;
   return FK_OK;
 }
@@ -384,6 +392,9 @@ int fk_add(fk_index* h, const void* x, int64_t n, int dtype, const int64_t* ids,
     iota_ids_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(h->ids + h->ntotal, h->ntotal, n);
     CKL();
   }
+  norm_max_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, st>>>(
+      h->norms + h->ntotal, n, reinterpret_cast<unsigned int*>(h->xn_max));
+  CKL();
   if (!on_device) CK(cudaStreamSynchronize(st));
   h->ntotal += n;
   return FK_OK;
@@ -491,6 +502,8 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
 
     if ((rc = h->pkey.ensure((size_t)nq * S_tot * k * sizeof(uint32_t)))) return rc;
     if ((rc = h->ppos.ensure((size_t)nq * S_tot * k * sizeof(uint32_t)))) return rc;
+    if ((rc = h->thr.ensure((size_t)nq * sizeof(uint32_t)))) return rc;
+    CK(cudaMemsetAsync(h->thr.p, 0xFF, (size_t)nq * sizeof(uint32_t), st));
 
     CUtensorMap ta0, ta1, tb0, tb1;
     const int eb = elem_bytes_of(h->storage);
@@ -506,8 +519,10 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
     SearchParams sp;
     sp.qnorm = static_cast<const float*>(h->qn.p);
     sp.xnorm = h->norms;
+    sp.xn_max = h->xn_max;
     sp.part_key = static_cast<uint32_t*>(h->pkey.p);
     sp.part_pos = static_cast<uint32_t*>(h->ppos.p);
+    sp.thr_key = static_cast<uint32_t*>(h->thr.p);
     sp.dbg_ip = h->dbg_ip;
     sp.nq = (int)nq;
     sp.nb = (int)h->ntotal;
@@ -519,6 +534,8 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
     sp.num_units = num_units;
     sp.num_kb = num_kb;
     sp.a_mode = a_mode;
+    sp.dbg_flags = 0;
+    if (const char* e = getenv("FK_DEBUG_FLAGS")) sp.dbg_flags = atoi(e);
     sp.qa0 = h->q0.p;
     sp.qa1 = h->q1.p;
     sp.stages = stages;

@@ -42,8 +42,10 @@ __device__ __forceinline__ float unmonotone(uint32_t k) {
 struct SearchParams {
   const float* qnorm;  // [nq]
   const float* xnorm;  // [cap], cap padded to BN
+  const float* xn_max; // device scalar: max stored norm (bounds the filter's rounding margin)
   uint32_t* part_key;  // [nq][S][k]
   uint32_t* part_pos;  // [nq][S][k]
+  uint32_t* thr_key;   // [nq] shared per-query bound: min over units of their k-th key
   float* dbg_ip;       // optional raw inner products [nq][nb] (debug)
   const void* qa0;     // query operand rows [nq][dp] (hi / f16 / bf16) -- A_TMEM mode
   const void* qa1;     // lo part (fp32 mode)
@@ -52,6 +54,7 @@ struct SearchParams {
   int num_kb;      // padded d / elements-per-128B-chunk
   int a_mode;      // 0: queries in TMEM, 1: resident in smem, 2: streamed per stage
   int stages;      // B (and streamed A) pipeline depth
+  int dbg_flags;   // bottleneck experiments: 1 = epilogue skips compute, 2 = producer skips TMA
 };
 
 // ------------------------------------------------------------ register queue
@@ -99,6 +102,22 @@ __device__ __forceinline__ void queue_insert(uint32_t (&keys)[KQ], uint32_t (&po
 // a_mode 1: queries resident in smem for the unit
 // a_mode 2: queries streamed with every B stage (large d)
 constexpr int TMEM_A_COL = 2 * BN;  // A operand columns start after the accumulators
+
+// NaN-propagating min / max over 32 values with 3-input FMNMX (16 instructions).
+template <bool MAX>
+__device__ __forceinline__ float reduce32(const float (&v)[32]) {
+  auto op3 = [](float a, float b, float c) { return MAX ? fmax3_nan(a, b, c) : fmin3_nan(a, b, c); };
+  auto op2 = [](float a, float b) { return MAX ? fmax_nan(a, b) : fmin_nan(a, b); };
+  float l1[11];
+#pragma unroll
+  for (int i = 0; i < 10; ++i) l1[i] = op3(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+  l1[10] = op2(v[30], v[31]);
+  const float a = op3(l1[0], l1[1], l1[2]);
+  const float b = op3(l1[3], l1[4], l1[5]);
+  const float c = op3(l1[6], l1[7], l1[8]);
+  const float d = op2(l1[9], l1[10]);
+  return op2(op3(a, b, c), d);
+}
 
 __device__ __forceinline__ float select32(const float (&s)[32], int j) {
   float t16[16], t8[8], t4[4], t2[2];
@@ -201,6 +220,14 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         for (int t = t0; t < t1; ++t) {
           for (int kb = 0; kb < num_kb; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1);
+            if (p.dbg_flags & 2) {  // experiment: no data movement
+              mbar_arrive(&full[stage]);
+              if (++stage == (uint32_t)stages) {
+                stage = 0;
+                phase ^= 1;
+              }
+              continue;
+            }
             mbar_arrive_expect_tx(&full[stage], stage_bytes);
             uint8_t* sb = st_region + stage * stage_bytes;
             tma_load_2d(sb, &tm_b0, &full[stage], kb * BK, t * BN, pol_b);
@@ -346,7 +373,19 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         keys[i] = (i < KQ - k) ? 0u : 0xFFFFFFFFu;
         pos[i] = 0xFFFFFFFFu;
       }
-      float thr = __uint_as_float(0x7FFFFFFFu);  // NaN: queue not full, everything passes
+      // Effective threshold = min(own k-th, best k-th published by any unit of
+      // this query): every true top-k member has key <= the global k-th <= it.
+      uint32_t gkey = row_ok ? __ldcg(p.thr_key + row) : 0xFFFFFFFFu;
+      float thr = unmonotone(gkey);  // NaN while nothing is known: everything passes
+      // Conservative fast-filter bound on f = fl(xn - 2ip): the reference value
+      // fl(fl(qn + xn) - 2ip) differs from qn + f by < 3u(qn + xn + |v|); the
+      // 2^-20 margin (u = 2^-24) over max-norm covers it with room to spare.
+      const float xmax = IS_IP ? 0.f : *p.xn_max;
+      auto filter_bound = [&](float th) -> float {
+        if (IS_IP) return th;
+        return (th - qn) + (qn + xmax + fabsf(th)) * 9.5367431640625e-07f;
+      };
+      float T = filter_bound(thr);
 
       for (int t = t0; t < t1; ++t, ++tcount) {
         const uint32_t buf = tcount & 1, tph = (tcount >> 1) & 1;
@@ -355,63 +394,79 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         tc_fence_after();
         const int n0 = t * BN + h * COLS;
         const int nvalid = p.nb - n0;
-#pragma unroll 1
-        for (int c = 0; c < COLS / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(tmem_base + lane_addr + buf * BN + h * COLS + c * 32, r);
-          tmem_ld_wait();
-          if (p.dbg_ip != nullptr && row_ok) {
-            for (int j = 0; j < 32; ++j)
-              if (c * 32 + j < nvalid) p.dbg_ip[(size_t)row * p.nb + n0 + c * 32 + j] = __uint_as_float(r[j]);
-          }
-          float s[32];
+        const float* xs = xn_s + buf * BN + h * COLS;
+        // Filter on f = xn - 2 ip (L2; one FMA) or -ip (IP) against T; the
+        // exact reference value (qn + xn) - 2 ip is computed for survivors only.
+        auto process = [&](const uint32_t (&r)[32], int c0) {
+          float f[32];
+          float m;
           if (IS_IP) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) s[j] = -__uint_as_float(r[j]);
+            for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(r[j]);
+            m = -reduce32<true>(f);  // min(-ip) = -max(ip)
           } else {
-            const float4* xs4 = reinterpret_cast<const float4*>(xn_s + buf * BN + h * COLS + c * 32);
+            const float4* xs4 = reinterpret_cast<const float4*>(xs + c0);
 #pragma unroll
             for (int j4 = 0; j4 < 8; ++j4) {
               const float4 x = xs4[j4];
-              // flat.py:111: (qn + norms) - 2.0*ip ; 2*ip is exact -> one FMA
-              s[4 * j4 + 0] = fmaf(-2.f, __uint_as_float(r[4 * j4 + 0]), qn + x.x);
-              s[4 * j4 + 1] = fmaf(-2.f, __uint_as_float(r[4 * j4 + 1]), qn + x.y);
-              s[4 * j4 + 2] = fmaf(-2.f, __uint_as_float(r[4 * j4 + 2]), qn + x.z);
-              s[4 * j4 + 3] = fmaf(-2.f, __uint_as_float(r[4 * j4 + 3]), qn + x.w);
+              f[4 * j4 + 0] = fmaf(-2.f, __uint_as_float(r[4 * j4 + 0]), x.x);
+              f[4 * j4 + 1] = fmaf(-2.f, __uint_as_float(r[4 * j4 + 1]), x.y);
+              f[4 * j4 + 2] = fmaf(-2.f, __uint_as_float(r[4 * j4 + 2]), x.z);
+              f[4 * j4 + 3] = fmaf(-2.f, __uint_as_float(r[4 * j4 + 3]), x.w);
             }
+            m = reduce32<false>(f);
           }
-          float mn[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) mn[i] = fmin_nan(s[2 * i], s[2 * i + 1]);
-#pragma unroll
-          for (int w = 8; w > 0; w >>= 1)
-#pragma unroll
-            for (int i = 0; i < w; ++i) mn[i] = fmin_nan(mn[i], mn[i + w]);
-          if (!(mn[0] > thr)) {
-            // rare path: exact (value, position) insertion of every survivor
-            const int lim = nvalid - c * 32;
-            uint32_t mask = lim >= 32 ? 0xFFFFFFFFu : (lim <= 0 ? 0u : ((1u << lim) - 1u));
+          if (!(m > T)) {
+            const int lim = nvalid - c0;
+            const uint32_t valid = lim >= 32 ? 0xFFFFFFFFu : (lim <= 0 ? 0u : ((1u << lim) - 1u));
             uint32_t cand = 0;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) cand |= (!(s[j] > thr) ? 1u : 0u) << j;
-            cand &= mask;
+            for (int j = 0; j < 32; ++j) cand |= ((IS_IP ? !(-f[j] > T) : !(f[j] > T)) ? 1u : 0u) << j;
+            cand &= valid;
             while (cand) {
               const int j = __ffs(cand) - 1;
               cand &= cand - 1;
-              float v = select32(s, j);
+              const float ip = select32(reinterpret_cast<const float(&)[32]>(r), j);
+              // flat.py:111: dmat = (qn + norms) - 2.0*ip  (2*ip exact -> one FMA)
+              float v = IS_IP ? -ip : fmaf(-2.f, ip, qn + xs[c0 + j]);
               if (!(v > thr)) {
                 if (!IS_IP) v = (v <= 0.f) ? 0.f : v;  // np.maximum(dmat, 0) (flat.py:112)
-                queue_insert<KQ>(keys, pos, monotone(v), static_cast<uint32_t>(n0 + c * 32 + j));
-                thr = unmonotone(keys[KQ - 1]);
+                queue_insert<KQ>(keys, pos, monotone(v), static_cast<uint32_t>(n0 + c0 + j));
+                thr = unmonotone(min(keys[KQ - 1], gkey));
+                T = filter_bound(thr);
               }
             }
           }
+        };
+#pragma unroll 1
+        for (int c = 0; c < ((p.dbg_flags & 1) ? 0 : COLS / 64); ++c) {
+          uint32_t ra[32], rb[32];
+          const uint32_t ta = tmem_base + lane_addr + buf * BN + h * COLS + c * 64;
+          tmem_ld_32x32b_x32(ta, ra);
+          tmem_ld_32x32b_x32(ta + 32, rb);
+          tmem_ld_wait();
+          if (p.dbg_ip != nullptr && row_ok) {
+            for (int j = 0; j < 32; ++j) {
+              if (c * 64 + j < nvalid) p.dbg_ip[(size_t)row * p.nb + n0 + c * 64 + j] = __uint_as_float(ra[j]);
+              if (c * 64 + 32 + j < nvalid)
+                p.dbg_ip[(size_t)row * p.nb + n0 + c * 64 + 32 + j] = __uint_as_float(rb[j]);
+            }
+          }
+          process(ra, c * 64);
+          process(rb, c * 64 + 32);
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[buf]);
+        if (((t - t0) & 15) == 15 && row_ok) {  // publish own k-th, fetch the shared bound
+          const uint32_t mine = keys[KQ - 1];
+          gkey = min(atomicMin(p.thr_key + row, mine), mine);
+          thr = unmonotone(min(keys[KQ - 1], gkey));
+          T = filter_bound(thr);
+        }
       }
       if (row_ok) {
+        atomicMin(p.thr_key + row, keys[KQ - 1]);
         const int S_tot = p.S * NH;
         const size_t base = ((size_t)row * S_tot + chunk * NH + h) * (size_t)k;
 #pragma unroll
@@ -619,6 +674,17 @@ __global__ void gather_rows_kernel(const uint8_t* __restrict__ src, uint8_t* __r
   uint8_t* o = dst + (size_t)i * row_bytes;
   for (size_t b = threadIdx.x * 4; b < row_bytes; b += blockDim.x * 4)
     *reinterpret_cast<uint32_t*>(o + b) = *reinterpret_cast<const uint32_t*>(s + b);
+}
+
+// Running max of non-negative float norms (uint compare == float compare for
+// x >= 0; a NaN norm wins, which disables the fast filter -- still exact).
+__global__ void norm_max_kernel(const float* __restrict__ norms, int64_t n, unsigned int* out) {
+  unsigned int m = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, __float_as_uint(fabsf(norms[i])) | (isnan(norms[i]) ? 0x7FC00000u : 0u));
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, off));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
 }
 
 __global__ void iota_ids_kernel(int64_t* ids, int64_t start, int64_t n) {
