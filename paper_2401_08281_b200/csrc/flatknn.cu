@@ -88,6 +88,8 @@ int make_map(CUtensorMap* m, const void* base, int elem_bytes, uint64_t cols, ui
   return FK_OK;
 }
 
+constexpr int FK_MAX_K = 2048;
+constexpr int MERGE_SMC = 8192;     // large-k merge: survivors sorted in smem (64 KB)
 constexpr int SMEM_LIMIT = 232448;  // sm_100 max dynamic smem per block (227 KB)
 constexpr int SMEM_RESERVE = 1024 /*align*/ + 2 * BN * 4 /*norm tiles*/ + 256 /*barriers + tmem slot*/;
 
@@ -127,7 +129,7 @@ struct fk_index {
   float* norms = nullptr;    // [cap]
   float* xn_max = nullptr;   // device scalar: max stored norm
   int64_t* ids = nullptr;    // [cap]
-  DevBuf q_in, q0, q1, qn, pkey, ppos, thr, outD, outI, outP, stage_in, stage_ids;
+  DevBuf q_in, q0, q1, qn, pkey, ppos, thr, pcnt, cbuf, outD, outI, outP, stage_in, stage_ids;
   std::mutex mu;
   int num_sms = 148;
   int profiling = 0;
@@ -233,6 +235,7 @@ int launch_fused_k(int kq, const CUtensorMap& a0, const CUtensorMap& a1, const C
     case 8: return launch_fused_t<MODE, 8, IP, EPI>(a0, a1, b0, b1, sp, grid, smem, st);
     case 16: return launch_fused_t<MODE, 16, IP, EPI>(a0, a1, b0, b1, sp, grid, smem, st);
     case 32: return launch_fused_t<MODE, 32, IP, EPI>(a0, a1, b0, b1, sp, grid, smem, st);
+    case 0: return launch_fused_t<MODE, 0, IP, EPI>(a0, a1, b0, b1, sp, grid, smem, st);
   }
   return set_err(FK_E_UNSUPPORTED, "queue bucket %d", kq);
 }
@@ -335,7 +338,7 @@ void fk_destroy(fk_index* h) {
   cudaFree(h->s1);
   cudaFree(h->norms);
   cudaFree(h->ids);
-  for (DevBuf* b : {&h->q_in, &h->q0, &h->q1, &h->qn, &h->pkey, &h->ppos, &h->thr, &h->outD, &h->outI, &h->outP,
+  for (DevBuf* b : {&h->q_in, &h->q0, &h->q1, &h->qn, &h->pkey, &h->ppos, &h->thr, &h->pcnt, &h->cbuf, &h->outD, &h->outI, &h->outP,
                     &h->stage_in, &h->stage_ids})
     b->release();
   cudaFree(h->xn_max);
@@ -443,7 +446,8 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
     if (k <= 8) kq = 8;
     else if (k <= 16) kq = 16;
     else if (k <= 32) kq = 32;
-    else return set_err(FK_E_UNSUPPORTED, "k=%d: the large-k selection path is not built yet (k <= 32)", k);
+    else if (k <= FK_MAX_K) kq = 0;  // large-k: candidate buffers + exact radix-select compaction
+    else return set_err(FK_E_UNSUPPORTED, "k=%d exceeds the maximum supported k (%d)", k, FK_MAX_K);
 
     // ---- queries -> device operand layout + norms
     const size_t in_row = (size_t)h->d * dtype_bytes(dtype);
@@ -485,8 +489,9 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
     int a_mode = a_tmem_cols <= 256 ? 0 : 1;
     if (const char* e = getenv("FK_FORCE_AMODE")) a_mode = std::max(0, std::min(2, atoi(e)));
     if (a_mode == 0 && a_tmem_cols > 256) a_mode = 1;
+    const int hist_bytes = kq == 0 ? epi * 1024 : 0;
     auto stages_for = [&](int mode) {
-      const int avail = SMEM_LIMIT - SMEM_RESERVE - (mode == 1 ? a_bytes : 0);
+      const int avail = SMEM_LIMIT - SMEM_RESERVE - hist_bytes - (mode == 1 ? a_bytes : 0);
       return avail / ((mode == 2 ? 2 : 1) * split * (int)CHUNK_BYTES);
     };
     int stages = stages_for(a_mode);
@@ -497,13 +502,20 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
     stages = std::min(stages, 8);
     if (const char* e = getenv("FK_STAGES")) stages = std::max(2, std::min(stages, atoi(e)));
     if (stages < 2) return set_err(FK_E_UNSUPPORTED, "pipeline does not fit in shared memory");
-    const int smem = SMEM_RESERVE + (a_mode == 1 ? a_bytes : 0) + stages * (a_mode == 2 ? 2 : 1) * split * (int)CHUNK_BYTES;
+    const int smem = SMEM_RESERVE + hist_bytes + (a_mode == 1 ? a_bytes : 0) +
+                     stages * (a_mode == 2 ? 2 : 1) * split * (int)CHUNK_BYTES;
     const int S_tot = S * nh;
 
     if ((rc = h->pkey.ensure((size_t)nq * S_tot * k * sizeof(uint32_t)))) return rc;
     if ((rc = h->ppos.ensure((size_t)nq * S_tot * k * sizeof(uint32_t)))) return rc;
     if ((rc = h->thr.ensure((size_t)nq * sizeof(uint32_t)))) return rc;
     CK(cudaMemsetAsync(h->thr.p, 0xFF, (size_t)nq * sizeof(uint32_t), st));
+    int cap = 0;
+    if (kq == 0) {
+      cap = (std::max(2 * k, k + 256) + 31) / 32 * 32;
+      if ((rc = h->pcnt.ensure((size_t)nq * S_tot * sizeof(int)))) return rc;
+      if ((rc = h->cbuf.ensure((size_t)grid * epi * 32 * cap * sizeof(uint64_t)))) return rc;
+    }
 
     CUtensorMap ta0, ta1, tb0, tb1;
     const int eb = elem_bytes_of(h->storage);
@@ -523,6 +535,9 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
     sp.part_key = static_cast<uint32_t*>(h->pkey.p);
     sp.part_pos = static_cast<uint32_t*>(h->ppos.p);
     sp.thr_key = static_cast<uint32_t*>(h->thr.p);
+    sp.part_cnt = static_cast<int*>(h->pcnt.p);
+    sp.cbuf = static_cast<uint64_t*>(h->cbuf.p);
+    sp.cap = cap;
     sp.dbg_ip = h->dbg_ip;
     sp.nq = (int)nq;
     sp.nb = (int)h->ntotal;
@@ -553,12 +568,31 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
     h->nlaunch++;
     if (ev) CK(cudaEventRecord(ev[2], st));
 
-    const int wpb = 8;
-    const unsigned mgrid = (unsigned)((nq + wpb - 1) / wpb);
-    if (ip)
-      merge_kernel<true><<<mgrid, wpb * 32, 0, st>>>(sp.part_key, sp.part_pos, S_tot, (int)nq, k, h->ids, dD, dI, dP);
-    else
-      merge_kernel<false><<<mgrid, wpb * 32, 0, st>>>(sp.part_key, sp.part_pos, S_tot, (int)nq, k, h->ids, dD, dI, dP);
+    if (kq == 0) {
+      int smc = MERGE_SMC;  // FK_MERGE_SMC (tests): lower the smem fast-path limit to exercise the radix fallback
+      if (const char* e = getenv("FK_MERGE_SMC")) smc = std::max(1, std::min(MERGE_SMC, atoi(e)));
+      static bool merge_cfg = false;
+      if (!merge_cfg) {
+        CK(cudaFuncSetAttribute(merge_large_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                MERGE_SMC * 8));
+        CK(cudaFuncSetAttribute(merge_large_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                MERGE_SMC * 8));
+        merge_cfg = true;
+      }
+      if (ip)
+        merge_large_kernel<true><<<(unsigned)nq, 256, MERGE_SMC * 8, st>>>(
+            sp.part_key, sp.part_pos, sp.part_cnt, S_tot, (int)nq, k, sp.thr_key, h->ids, dD, dI, dP, smc);
+      else
+        merge_large_kernel<false><<<(unsigned)nq, 256, MERGE_SMC * 8, st>>>(
+            sp.part_key, sp.part_pos, sp.part_cnt, S_tot, (int)nq, k, sp.thr_key, h->ids, dD, dI, dP, smc);
+    } else {
+      const int wpb = 8;
+      const unsigned mgrid = (unsigned)((nq + wpb - 1) / wpb);
+      if (ip)
+        merge_kernel<true><<<mgrid, wpb * 32, 0, st>>>(sp.part_key, sp.part_pos, S_tot, (int)nq, k, h->ids, dD, dI, dP);
+      else
+        merge_kernel<false><<<mgrid, wpb * 32, 0, st>>>(sp.part_key, sp.part_pos, S_tot, (int)nq, k, h->ids, dD, dI, dP);
+    }
     CKL();
     h->nlaunch++;
     if (ev) CK(cudaEventRecord(ev[3], st));

@@ -46,6 +46,9 @@ struct SearchParams {
   uint32_t* part_key;  // [nq][S][k]
   uint32_t* part_pos;  // [nq][S][k]
   uint32_t* thr_key;   // [nq] shared per-query bound: min over units of their k-th key
+  int* part_cnt;       // [nq][S_tot] valid entries per partial list (large-k mode)
+  uint64_t* cbuf;      // large-k candidate buffers [grid][EPI][32][cap] of (key<<32 | pos)
+  int cap;             // large-k buffer capacity per row
   float* dbg_ip;       // optional raw inner products [nq][nb] (debug)
   const void* qa0;     // query operand rows [nq][dp] (hi / f16 / bf16) -- A_TMEM mode
   const void* qa1;     // lo part (fp32 mode)
@@ -82,6 +85,100 @@ __device__ __forceinline__ void queue_insert(uint32_t (&keys)[KQ], uint32_t (&po
       pos[0] = p;
     }
   }
+}
+
+// ------------------------------------------------------------ exact selection (large k)
+constexpr unsigned FULLMASK = 0xFFFFFFFFu;
+
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const uint64_t o = __shfl_xor_sync(FULLMASK, v, off);
+    v = o < v ? o : v;
+  }
+  return v;
+}
+
+// Exact k-th smallest (1-based) of cnt 64-bit composites (key<<32 | position)
+// read through load(e): warp-cooperative MSB-first 8-bit radix select with a
+// 256-bin smem histogram; stops as soon as the k-th is alone in its bucket.
+template <class Load>
+__device__ uint64_t warp_kth(Load load, int cnt, uint32_t k, uint32_t* hist) {
+  const int lane = threadIdx.x & 31;
+  uint64_t prefix = 0;
+  uint32_t need = k;
+#pragma unroll 1
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    const uint64_t hmask = (shift == 56) ? 0ull : (~0ull << (shift + 8));
+    for (int b = lane; b < 256; b += 32) hist[b] = 0;
+    __syncwarp();
+    for (int e = lane; e < cnt; e += 32) {
+      const uint64_t v = load(e);
+      if ((v & hmask) == prefix) atomicAdd(&hist[static_cast<uint32_t>(v >> shift) & 255u], 1u);
+    }
+    __syncwarp();
+    uint32_t c[8], sum = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      c[i] = hist[lane * 8 + i];
+      sum += c[i];
+    }
+    uint32_t incl = sum;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t o = __shfl_up_sync(FULLMASK, incl, off);
+      if (lane >= off) incl += o;
+    }
+    const uint32_t excl = incl - sum;
+    const unsigned own = __ballot_sync(FULLMASK, excl < need && need <= incl);
+    const int src = own ? __ffs(own) - 1 : 31;
+    uint32_t bin = 0, before = 0, bcnt = 0;
+    if (lane == src) {
+      uint32_t run = excl;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (bcnt == 0 && run < need && need <= run + c[i]) {
+          bin = lane * 8 + i;
+          before = run;
+          bcnt = c[i];
+        }
+        run += c[i];
+      }
+    }
+    bin = __shfl_sync(FULLMASK, bin, src);
+    before = __shfl_sync(FULLMASK, before, src);
+    bcnt = __shfl_sync(FULLMASK, bcnt, src);
+    need -= before;
+    prefix |= static_cast<uint64_t>(bin) << shift;
+    __syncwarp();
+    if (bcnt == 1) {  // the k-th is the only value in its bucket
+      const uint64_t m2 = ~0ull << shift;
+      uint64_t found = ~0ull;
+      for (int e = lane; e < cnt; e += 32) {
+        const uint64_t v = load(e);
+        if ((v & m2) == prefix) found = v;
+      }
+      return warp_min_u64(found);
+    }
+  }
+  return prefix;
+}
+
+// In-place, order-preserving compaction of buf[0..cnt) to the values <= kth.
+__device__ __forceinline__ int warp_compact_le(uint64_t* buf, int cnt, uint64_t kth) {
+  const int lane = threadIdx.x & 31;
+  int out = 0;
+  for (int base = 0; base < cnt; base += 32) {
+    const int e = base + lane;
+    const uint64_t v = e < cnt ? buf[e] : ~0ull;
+    const bool keep = e < cnt && v <= kth;
+    const unsigned b = __ballot_sync(FULLMASK, keep);
+    __syncwarp();
+    if (keep) buf[out + __popc(b & ((1u << lane) - 1u))] = v;
+    out += __popc(b);
+    __syncwarp();
+  }
+  return out;
 }
 
 // ------------------------------------------------------------ fused kernel
@@ -159,7 +256,8 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
   uint8_t* a_region = smem;
   uint8_t* st_region = smem + a_bytes;
   float* xn_s = reinterpret_cast<float*>(st_region + stages * stage_bytes);  // [2][BN]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(xn_s + 2 * BN);
+  uint32_t* hist_base = reinterpret_cast<uint32_t*>(xn_s + 2 * BN);  // large-k: [EPI][256]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(hist_base + (KQ == 0 ? EPI * 256 : 0));
   uint64_t* full = bars;
   uint64_t* empty = bars + stages;
   uint64_t* tfull = bars + 2 * stages;
@@ -367,12 +465,25 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       }
 
       const float qn = (!IS_IP && row_ok) ? p.qnorm[row] : 0.f;
-      uint32_t keys[KQ], pos[KQ];
+      constexpr int KQS = KQ > 0 ? KQ : 1;
+      uint32_t keys[KQS], pos[KQS];
+      if constexpr (KQ > 0) {
 #pragma unroll
-      for (int i = 0; i < KQ; ++i) {
-        keys[i] = (i < KQ - k) ? 0u : 0xFFFFFFFFu;
-        pos[i] = 0xFFFFFFFFu;
+        for (int i = 0; i < KQ; ++i) {
+          keys[i] = (i < KQ - k) ? 0u : 0xFFFFFFFFu;
+          pos[i] = 0xFFFFFFFFu;
+        }
       }
+      // large k: unsorted per-row candidate buffer + exact compaction
+      uint64_t* mybuf = nullptr;
+      int cnt = 0;
+      uint32_t lkey = 0xFFFFFFFFu;  // key of the k-th after the last compaction
+      uint32_t* hist = hist_base + ew * 256;
+      if constexpr (KQ == 0) mybuf = p.cbuf + (((size_t)blockIdx.x * EPI + ew) * 32 + lane) * (size_t)p.cap;
+      auto own_key = [&]() -> uint32_t {
+        if constexpr (KQ > 0) return keys[KQS - 1];
+        return lkey;
+      };
       // Effective threshold = min(own k-th, best k-th published by any unit of
       // this query): every true top-k member has key <= the global k-th <= it.
       uint32_t gkey = row_ok ? __ldcg(p.thr_key + row) : 0xFFFFFFFFu;
@@ -386,6 +497,25 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         return (th - qn) + (qn + xmax + fabsf(th)) * 9.5367431640625e-07f;
       };
       float T = filter_bound(thr);
+      // warp-uniform: compact every lane whose buffer holds more than `limit`
+      auto compact_lanes = [&](int limit) {
+        unsigned todo = __ballot_sync(FULLMASK, cnt > limit);
+        while (todo) {
+          const int L = __ffs(todo) - 1;
+          todo &= todo - 1;
+          const int cL = __shfl_sync(FULLMASK, cnt, L);
+          uint64_t* bL = reinterpret_cast<uint64_t*>(
+              __shfl_sync(FULLMASK, reinterpret_cast<unsigned long long>(mybuf), L));
+          const uint64_t kth = warp_kth([&](int e) { return bL[e]; }, cL, (uint32_t)k, hist);
+          const int nc = warp_compact_le(bL, cL, kth);
+          if (lane == L) {
+            cnt = nc;
+            lkey = static_cast<uint32_t>(kth >> 32);
+            thr = unmonotone(min(lkey, gkey));
+            T = filter_bound(thr);
+          }
+        }
+      };
 
       for (int t = t0; t < t1; ++t, ++tcount) {
         const uint32_t buf = tcount & 1, tph = (tcount >> 1) & 1;
@@ -416,7 +546,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             }
             m = reduce32<false>(f);
           }
-          if (!(m > T)) {
+          if (!(m > T) && row_ok) {
             const int lim = nvalid - c0;
             const uint32_t valid = lim >= 32 ? 0xFFFFFFFFu : (lim <= 0 ? 0u : ((1u << lim) - 1u));
             uint32_t cand = 0;
@@ -431,9 +561,13 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
               float v = IS_IP ? -ip : fmaf(-2.f, ip, qn + xs[c0 + j]);
               if (!(v > thr)) {
                 if (!IS_IP) v = (v <= 0.f) ? 0.f : v;  // np.maximum(dmat, 0) (flat.py:112)
-                queue_insert<KQ>(keys, pos, monotone(v), static_cast<uint32_t>(n0 + c0 + j));
-                thr = unmonotone(min(keys[KQ - 1], gkey));
-                T = filter_bound(thr);
+                if constexpr (KQ > 0) {
+                  queue_insert<KQS>(keys, pos, monotone(v), static_cast<uint32_t>(n0 + c0 + j));
+                  thr = unmonotone(min(keys[KQS - 1], gkey));
+                  T = filter_bound(thr);
+                } else {
+                  mybuf[cnt++] = (static_cast<uint64_t>(monotone(v)) << 32) | static_cast<uint32_t>(n0 + c0 + j);
+                }
               }
             }
           }
@@ -454,27 +588,41 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
           }
           process(ra, c * 64);
           process(rb, c * 64 + 32);
+          if constexpr (KQ == 0) compact_lanes(p.cap - 64);  // room for the next 64 columns
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[buf]);
         if (((t - t0) & 15) == 15 && row_ok) {  // publish own k-th, fetch the shared bound
-          const uint32_t mine = keys[KQ - 1];
+          const uint32_t mine = own_key();
           gkey = min(atomicMin(p.thr_key + row, mine), mine);
-          thr = unmonotone(min(keys[KQ - 1], gkey));
+          thr = unmonotone(min(mine, gkey));
           T = filter_bound(thr);
         }
       }
-      if (row_ok) {
-        atomicMin(p.thr_key + row, keys[KQ - 1]);
-        const int S_tot = p.S * NH;
-        const size_t base = ((size_t)row * S_tot + chunk * NH + h) * (size_t)k;
+      const int S_tot = p.S * NH;
+      const size_t base = ((size_t)row * S_tot + chunk * NH + h) * (size_t)k;
+      if constexpr (KQ > 0) {
+        if (row_ok) {
+          atomicMin(p.thr_key + row, keys[KQ - 1]);
 #pragma unroll
-        for (int i = 0; i < KQ; ++i) {
-          if (i >= KQ - k) {
-            p.part_key[base + i - (KQ - k)] = keys[i];
-            p.part_pos[base + i - (KQ - k)] = pos[i];
+          for (int i = 0; i < KQ; ++i) {
+            if (i >= KQ - k) {
+              p.part_key[base + i - (KQ - k)] = keys[i];
+              p.part_pos[base + i - (KQ - k)] = pos[i];
+            }
           }
+        }
+      } else {
+        compact_lanes(k);  // exact top-k of this unit's survivors
+        if (row_ok) {
+          if (lkey != 0xFFFFFFFFu) atomicMin(p.thr_key + row, lkey);
+          for (int i = 0; i < cnt; ++i) {
+            const uint64_t v = mybuf[i];
+            p.part_key[base + i] = static_cast<uint32_t>(v >> 32);
+            p.part_pos[base + i] = static_cast<uint32_t>(v);
+          }
+          p.part_cnt[(size_t)row * S_tot + chunk * NH + h] = cnt;
         }
       }
     }
@@ -489,15 +637,6 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
 }
 
 // ------------------------------------------------------------ merges
-__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    const uint64_t o = __shfl_xor_sync(0xFFFFFFFFu, v, off);
-    v = o < v ? o : v;
-  }
-  return v;
-}
-
 // One warp per query: k rounds of a warp-wide argmin over the heads of S
 // sorted partial lists (lane l owns lists l, l+32, l+64, l+96 -> S <= 128).
 template <bool IS_IP>
@@ -592,6 +731,102 @@ __global__ void shard_merge_kernel(int nshard, int nq, int k, const float* __res
         D[o] = IS_IP ? -v : v;
         I[o] = wid;
       }
+    }
+  }
+}
+
+
+// Large-k final merge: one CTA per query.  Survivors of every partial list
+// with key <= the query's final shared bound (>= k of them, and a superset of
+// the true top-k) are gathered into smem and bitonic-sorted by (key, position);
+// if they do not fit, an exact radix select over the lists picks the k-th first.
+template <bool IS_IP>
+__global__ void __launch_bounds__(256) merge_large_kernel(const uint32_t* __restrict__ pkey,
+                                                          const uint32_t* __restrict__ ppos,
+                                                          const int* __restrict__ pcnt, int S, int nq, int k,
+                                                          const uint32_t* __restrict__ thr_key,
+                                                          const int64_t* __restrict__ ids, float* __restrict__ D,
+                                                          int64_t* __restrict__ I, int64_t* __restrict__ P,
+                                                          int smc) {
+  extern __shared__ uint64_t sm[];
+  __shared__ int count;
+  __shared__ uint32_t hist[256];
+  __shared__ uint64_t kth_s;
+  const int q = blockIdx.x;
+  const int tid = threadIdx.x;
+  if (q >= nq) return;
+  const uint32_t thr = thr_key[q];
+  const uint32_t* lk = pkey + (size_t)q * S * k;
+  const uint32_t* lp = ppos + (size_t)q * S * k;
+  const int* lc = pcnt + (size_t)q * S;
+  if (tid == 0) count = 0;
+  __syncthreads();
+  const int total = S * k;
+  auto load = [&](int e) -> uint64_t {
+    const int s = e / k, i = e - s * k;
+    if (i >= lc[s]) return ~0ull;
+    const uint32_t key = lk[e];
+    if (key > thr) return ~0ull;
+    return (static_cast<uint64_t>(key) << 32) | lp[e];
+  };
+  for (int e = tid; e < total; e += blockDim.x) {
+    const uint64_t v = load(e);
+    if (v != ~0ull) {
+      const int idx = atomicAdd(&count, 1);
+      if (idx < smc) sm[idx] = v;
+    }
+  }
+  __syncthreads();
+  int n = count;
+  if (n > smc) {  // rare (massive exact ties): exact k-th first, then gather exactly k
+    if (tid < 32) {
+      const uint64_t kth = warp_kth(load, total, (uint32_t)min(k, n), hist);
+      if (tid == 0) {
+        kth_s = kth;
+        count = 0;
+      }
+    }
+    __syncthreads();
+    const uint64_t kth = kth_s;
+    for (int e = tid; e < total; e += blockDim.x) {
+      const uint64_t v = load(e);
+      if (v != ~0ull && v <= kth) sm[atomicAdd(&count, 1)] = v;
+    }
+    __syncthreads();
+    n = count;
+  }
+  int P2 = 1;
+  while (P2 < n) P2 <<= 1;
+  for (int i = n + tid; i < P2; i += blockDim.x) sm[i] = ~0ull;
+  __syncthreads();
+  for (int size = 2; size <= P2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = tid; i < P2 / 2; i += blockDim.x) {
+        const int lo = 2 * i - (i & (stride - 1));
+        const int hi = lo + stride;
+        const bool asc = (lo & size) == 0;
+        const uint64_t a = sm[lo], b = sm[hi];
+        if ((a > b) == asc) {
+          sm[lo] = b;
+          sm[hi] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int r = tid; r < k; r += blockDim.x) {
+    const size_t o = (size_t)q * k + r;
+    const uint64_t w = r < n ? sm[r] : ~0ull;
+    if (w == ~0ull) {
+      D[o] = IS_IP ? -INFINITY : INFINITY;
+      I[o] = -1;
+      if (P) P[o] = -1;
+    } else {
+      const uint32_t ps = static_cast<uint32_t>(w);
+      const float v = unmonotone(static_cast<uint32_t>(w >> 32));
+      D[o] = IS_IP ? -v : v;
+      I[o] = ids[ps];
+      if (P) P[o] = ps;
     }
   }
 }

@@ -35,12 +35,18 @@ for v in variants:
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / n
+    idx.set_profiling(True)
+    idx.kernel_times()
+    for _ in range(3):
+        idx.search(q, cfg["k"])
+    (tp, tf, tm), nl = idx.kernel_times()
+    idx.set_profiling(False)
     same = None
     if ref is None:
         ref = (r.ids.clone(), r.distances.clone())
     else:
         same = bool(torch.equal(ref[0], r.ids) and torch.equal(ref[1], r.distances))
-    print(json.dumps({"variant": v, "ms": round(ms, 3), "qps": round(cfg["nq"] / ms * 1e3), "plan": idx.last_plan(),
+    print(json.dumps({"variant": v, "ms": round(ms, 3), "prep_fused_merge_ms": [round(tp, 3), round(tf, 3), round(tm, 3)], "qps": round(cfg["nq"] / ms * 1e3), "plan": idx.last_plan(),
                       "same_as_first": same}), flush=True)
     for a in env:
         del os.environ[a]

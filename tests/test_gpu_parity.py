@@ -42,13 +42,7 @@ def build_index(name):
 @pytest.mark.parametrize("name", sorted(CASES))
 def test_golden_case(golden, name):
     idx, q, k = build_index(name)
-    if name in LARGE_K and CASES[name]["k"] > 32:
-        try:
-            res = idx.search(q, k)
-        except NotImplementedError:
-            pytest.skip("large-k path not built")
-    else:
-        res = idx.search(q, k)
+    res = idx.search(q, k)
     assert res.ids.shape == (q.shape[0], k) and res.ids.dtype == np.int64
     assert res.distances.dtype == np.float32
     s = assert_parity(res.ids, res.distances, golden[f"{name}/blas_ids"], golden[f"{name}/blas_dist"])
@@ -247,3 +241,61 @@ def test_cfg2_parity_vs_oracle_subset(cfg2_index):
     want_ids, want_dist = O.flat_search_blas(xb, q[sub], 10, "l2")
     s = assert_parity(res.ids.cpu().numpy()[sub], res.distances.cpu().numpy()[sub], want_ids, want_dist)
     assert s["strict_recall"] >= 0.999
+
+
+# ---------------------------------------------------------------- large k (candidate buffers + radix select)
+@pytest.mark.parametrize("k,metric,data", [(33, "l2", "gauss"), (100, "ip", "gauss"), (257, "l2", "ints"),
+                                           (1024, "l2", "gauss"), (2048, "ip", "gauss"), (1000, "l2", "ints")])
+def test_large_k_vs_oracle(k, metric, data):
+    rng = np.random.default_rng(k)
+    if data == "ints":  # massive exact ties: exercises (key, position) ordering in compaction and merge
+        xb = rng.integers(0, 3, size=(9000, 24)).astype(np.float32)
+        q = rng.integers(0, 3, size=(70, 24)).astype(np.float32)
+    else:
+        xb = rng.standard_normal((12000, 72), dtype=np.float32)
+        q = rng.standard_normal((150, 72), dtype=np.float32)
+    idx = FlatIndex(xb.shape[1], METRIC_L2 if metric == "l2" else METRIC_IP)
+    idx.add(xb)
+    res = idx.search(q, k)
+    want_ids, want_dist = O.flat_search_blas(xb, q, k, metric)
+    assert_parity(res.ids, res.distances, want_ids, want_dist)
+    if data == "ints":  # integer data: exact arithmetic on both sides -> identical order
+        assert np.array_equal(res.ids, want_ids)
+
+
+@pytest.mark.parametrize("force", [("FK_FORCE_S", "1"), ("FK_FORCE_S", "40"), ("FK_EPI", "8"),
+                                   ("FK_MERGE_SMC", "64"), ("FK_FORCE_AMODE", "2")])
+def test_large_k_plan_invariance(force):
+    rng = np.random.default_rng(7)
+    xb = rng.integers(0, 5, size=(30000, 40)).astype(np.float32)
+    q = rng.integers(0, 5, size=(200, 40)).astype(np.float32)
+    idx = IndexFlatL2(40)
+    idx.add(xb)
+    base = idx.search(q, 300)
+    os.environ[force[0]] = force[1]
+    try:
+        alt = idx.search(q, 300)
+    finally:
+        del os.environ[force[0]]
+    assert np.array_equal(base.ids, alt.ids) and np.array_equal(base.distances, alt.distances)
+    want_ids, _ = O.flat_search_blas(xb, q, 300, "l2")
+    assert np.array_equal(base.ids, want_ids)
+
+
+def test_k_equals_ntotal_large():
+    rng = np.random.default_rng(1)
+    idx = IndexFlatL2(4)
+    xb = rng.normal(size=(64, 4)).astype(np.float32)
+    idx.add(xb)
+    res = idx.search(rng.normal(size=(5, 4)).astype(np.float32), 64)
+    for row in res.ids:
+        assert sorted(row.tolist()) == list(range(64))
+    res = idx.search(xb[:3], 100)  # k > ntotal pads -1 / +inf
+    assert np.all(res.ids[:, 64:] == -1) and np.all(np.isinf(res.distances[:, 64:]))
+
+
+def test_k_above_max_rejected():
+    idx = IndexFlatL2(4)
+    idx.add(np.zeros((10, 4), np.float32))
+    with pytest.raises(NotImplementedError):
+        idx.search(np.zeros((1, 4), np.float32), 4096)
