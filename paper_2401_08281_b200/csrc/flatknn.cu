@@ -89,7 +89,7 @@ int make_map(CUtensorMap* m, const void* base, int elem_bytes, uint64_t cols, ui
 }
 
 constexpr int FK_MAX_K = 2048;
-constexpr int MERGE_SMC = 8192;     // large-k merge: survivors sorted in smem (64 KB)
+constexpr int MERGE_SMC = 16384;    // large-k merge: survivors gathered in smem (128 KB) + 2048 winners
 constexpr int SMEM_LIMIT = 232448;  // sm_100 max dynamic smem per block (227 KB)
 constexpr int SMEM_RESERVE = 1024 /*align*/ + 2 * BN * 4 /*norm tiles*/ + 256 /*barriers + tmem slot*/;
 
@@ -129,7 +129,8 @@ struct fk_index {
   float* norms = nullptr;    // [cap]
   float* xn_max = nullptr;   // device scalar: max stored norm
   int64_t* ids = nullptr;    // [cap]
-  DevBuf q_in, q0, q1, qn, pkey, ppos, thr, pcnt, cbuf, outD, outI, outP, stage_in, stage_ids;
+  DevBuf q_in, q0, q1, qn, pkey, ppos, thr, pcnt, cbuf, fail, outD, outI, outP, stage_in, stage_ids;
+  long long est_fallbacks = 0;  // large-k searches whose estimated bound failed certification
   std::mutex mu;
   int num_sms = 148;
   int profiling = 0;
@@ -338,7 +339,7 @@ void fk_destroy(fk_index* h) {
   cudaFree(h->s1);
   cudaFree(h->norms);
   cudaFree(h->ids);
-  for (DevBuf* b : {&h->q_in, &h->q0, &h->q1, &h->qn, &h->pkey, &h->ppos, &h->thr, &h->pcnt, &h->cbuf, &h->outD, &h->outI, &h->outP,
+  for (DevBuf* b : {&h->q_in, &h->q0, &h->q1, &h->qn, &h->pkey, &h->ppos, &h->thr, &h->pcnt, &h->cbuf, &h->fail, &h->outD, &h->outI, &h->outP,
                     &h->stage_in, &h->stage_ids})
     b->release();
   cudaFree(h->xn_max);
@@ -403,6 +404,153 @@ int fk_add(fk_index* h, const void* x, int64_t n, int dtype, const int64_t* ids,
   return FK_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+struct Plan {
+  int kq, epi, nh, num_m, n_tiles, S, chunk_tiles, num_units, grid, a_mode, stages, smem, S_tot, cap;
+};
+
+// Tile / split-N / pipeline plan for one fused pass over base rows [0, nb_pass).
+int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force_S, Plan* pl) {
+  Plan P{};
+  P.kq = kq;
+  P.epi = 4;
+  if (const char* e = getenv("FK_EPI")) P.epi = atoi(e) == 8 ? 8 : 4;
+  P.nh = P.epi / 4;
+  P.num_m = (int)((nq + BM - 1) / BM);
+  P.n_tiles = (int)((nb_pass + BN - 1) / BN);
+  plan_split(P.num_m, P.n_tiles, h->num_sms, 128 / P.nh, &P.S, &P.chunk_tiles);
+  int fs = force_S;
+  if (const char* e = getenv("FK_FORCE_S"); e && !force_S) fs = atoi(e);
+  if (fs > 0) {
+    P.S = std::max(1, std::min(fs, std::min(128 / P.nh, P.n_tiles)));
+    P.chunk_tiles = (P.n_tiles + P.S - 1) / P.S;
+    P.S = (P.n_tiles + P.chunk_tiles - 1) / P.chunk_tiles;
+  }
+  P.num_units = P.num_m * P.S;
+  P.grid = std::min(P.num_units, h->num_sms);
+  const int split = split_of(h->storage);
+  const int num_kb = h->dp / chunk_elems_of(h->storage);
+  const int a_bytes = split * num_kb * (int)CHUNK_BYTES;
+  const int a_tmem_cols = h->storage == FK_F32 ? 2 * h->dp : h->dp / 2;
+  P.a_mode = a_tmem_cols <= 256 ? 0 : 1;
+  if (const char* e = getenv("FK_FORCE_AMODE")) P.a_mode = std::max(0, std::min(2, atoi(e)));
+  if (P.a_mode == 0 && a_tmem_cols > 256) P.a_mode = 1;
+  const int hist_bytes = kq == 0 ? P.epi * 1024 : 0;
+  auto stages_for = [&](int mode) {
+    const int avail = SMEM_LIMIT - SMEM_RESERVE - hist_bytes - (mode == 1 ? a_bytes : 0);
+    return avail / ((mode == 2 ? 2 : 1) * split * (int)CHUNK_BYTES);
+  };
+  P.stages = stages_for(P.a_mode);
+  if (P.a_mode == 1 && P.stages < 3) {
+    P.a_mode = 2;
+    P.stages = stages_for(2);
+  }
+  P.stages = std::min(P.stages, 8);
+  if (const char* e = getenv("FK_STAGES")) P.stages = std::max(2, std::min(P.stages, atoi(e)));
+  if (P.stages < 2) return set_err(FK_E_UNSUPPORTED, "pipeline does not fit in shared memory");
+  P.smem = SMEM_RESERVE + hist_bytes + (P.a_mode == 1 ? a_bytes : 0) +
+           P.stages * (P.a_mode == 2 ? 2 : 1) * split * (int)CHUNK_BYTES;
+  P.S_tot = P.S * P.nh;
+  P.cap = kq == 0 ? (std::max(2 * k, k + 256) + 31) / 32 * 32 : 0;
+  *pl = P;
+  return FK_OK;
+}
+
+// One fused GEMM + top-k pass over base rows [0, nb_pass) for the prepared
+// queries; partial lists land in h->pkey/ppos (+pcnt), bounds in h->thr.
+int run_fused(fk_index* h, const Plan& P, int64_t nq, int64_t nb_pass, int k, bool ip, cudaStream_t st) {
+  int rc;
+  if ((rc = h->pkey.ensure((size_t)nq * P.S_tot * k * sizeof(uint32_t)))) return rc;
+  if ((rc = h->ppos.ensure((size_t)nq * P.S_tot * k * sizeof(uint32_t)))) return rc;
+  if (P.kq == 0) {
+    if ((rc = h->pcnt.ensure((size_t)nq * P.S_tot * sizeof(int)))) return rc;
+    if ((rc = h->cbuf.ensure((size_t)P.grid * P.epi * 32 * P.cap * sizeof(uint64_t)))) return rc;
+  }
+  CUtensorMap ta0, ta1, tb0, tb1;
+  const int eb = elem_bytes_of(h->storage);
+  if ((rc = make_map(&ta0, h->q0.p, eb, h->dp, nq))) return rc;
+  if ((rc = make_map(&tb0, h->s0, eb, h->dp, nb_pass))) return rc;
+  if (h->storage == FK_F32) {
+    if ((rc = make_map(&ta1, h->q1.p, eb, h->dp, nq))) return rc;
+    if ((rc = make_map(&tb1, h->s1, eb, h->dp, nb_pass))) return rc;
+  } else {
+    ta1 = ta0;
+    tb1 = tb0;
+  }
+  SearchParams sp;
+  std::memset(&sp, 0, sizeof(sp));
+  sp.qnorm = static_cast<const float*>(h->qn.p);
+  sp.xnorm = h->norms;
+  sp.xn_max = h->xn_max;
+  sp.part_key = static_cast<uint32_t*>(h->pkey.p);
+  sp.part_pos = static_cast<uint32_t*>(h->ppos.p);
+  sp.thr_key = static_cast<uint32_t*>(h->thr.p);
+  sp.part_cnt = static_cast<int*>(h->pcnt.p);
+  sp.cbuf = static_cast<uint64_t*>(h->cbuf.p);
+  sp.cap = P.cap;
+  sp.dbg_ip = h->dbg_ip;
+  sp.qa0 = h->q0.p;
+  sp.qa1 = h->q1.p;
+  sp.nq = (int)nq;
+  sp.nb = (int)nb_pass;
+  sp.k = k;
+  sp.num_m = P.num_m;
+  sp.n_tiles = P.n_tiles;
+  sp.chunk_tiles = P.chunk_tiles;
+  sp.S = P.S;
+  sp.num_units = P.num_units;
+  sp.num_kb = h->dp / chunk_elems_of(h->storage);
+  sp.a_mode = P.a_mode;
+  sp.stages = P.stages;
+  if (const char* e = getenv("FK_DEBUG_FLAGS")) sp.dbg_flags = atoi(e);
+  rc = launch_fused(P.epi, h->storage, ip, P.kq, ta0, ta1, tb0, tb1, sp, P.grid, P.smem, st);
+  if (rc == FK_OK) h->nlaunch++;
+  return rc;
+}
+
+int launch_merge(fk_index* h, const Plan& P, int64_t nq, int k, bool ip, float* dD, int64_t* dI, int64_t* dP,
+                 int* fail, cudaStream_t st) {
+  const uint32_t* pk = static_cast<const uint32_t*>(h->pkey.p);
+  const uint32_t* pp = static_cast<const uint32_t*>(h->ppos.p);
+  if (P.kq == 0) {
+    int smc = MERGE_SMC;  // FK_MERGE_SMC (tests): lower the smem fast-path limit to exercise the radix fallback
+    if (const char* e = getenv("FK_MERGE_SMC")) smc = std::max(1, std::min(MERGE_SMC, atoi(e)));
+    static bool merge_cfg = false;
+    if (!merge_cfg) {
+      CK(cudaFuncSetAttribute(merge_large_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (MERGE_SMC + FK_MAX_K) * 8));
+      CK(cudaFuncSetAttribute(merge_large_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (MERGE_SMC + FK_MAX_K) * 8));
+      merge_cfg = true;
+    }
+    const int* pc = static_cast<const int*>(h->pcnt.p);
+    const uint32_t* thr = static_cast<const uint32_t*>(h->thr.p);
+    if (ip)
+      merge_large_kernel<true><<<(unsigned)nq, 256, (smc + FK_MAX_K) * 8, st>>>(pk, pp, pc, P.S_tot, (int)nq, k, thr,
+                                                                              h->ids, dD, dI, dP, smc, fail);
+    else
+      merge_large_kernel<false><<<(unsigned)nq, 256, (smc + FK_MAX_K) * 8, st>>>(pk, pp, pc, P.S_tot, (int)nq, k, thr,
+                                                                               h->ids, dD, dI, dP, smc, fail);
+  } else {
+    const int wpb = 8;
+    const unsigned mgrid = (unsigned)((nq + wpb - 1) / wpb);
+    if (ip)
+      merge_kernel<true><<<mgrid, wpb * 32, 0, st>>>(pk, pp, P.S_tot, (int)nq, k, h->ids, dD, dI, dP);
+    else
+      merge_kernel<false><<<mgrid, wpb * 32, 0, st>>>(pk, pp, P.S_tot, (int)nq, k, h->ids, dD, dI, dP);
+  }
+  CKL();
+  h->nlaunch++;
+  return FK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D, int64_t* I, int64_t* P,
               int on_device, void* stream) {
   if (!h) return set_err(FK_E_INVALID, "NULL index");
@@ -412,6 +560,7 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
   if (nq == 0) return FK_OK;
   if (!q || !D || !I) return set_err(FK_E_INVALID, "NULL query/output pointer");
   if (nq > (int64_t)INT32_MAX / 2) return set_err(FK_E_UNSUPPORTED, "nq too large for one call");
+  if (k > FK_MAX_K) return set_err(FK_E_UNSUPPORTED, "k=%d exceeds the maximum supported k (%d)", k, FK_MAX_K);
   std::lock_guard<std::mutex> g(h->mu);
   CK(cudaSetDevice(h->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -442,12 +591,7 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
     CKL();
     h->nlaunch = 1;
   } else {
-    int kq;
-    if (k <= 8) kq = 8;
-    else if (k <= 16) kq = 16;
-    else if (k <= 32) kq = 32;
-    else if (k <= FK_MAX_K) kq = 0;  // large-k: candidate buffers + exact radix-select compaction
-    else return set_err(FK_E_UNSUPPORTED, "k=%d exceeds the maximum supported k (%d)", k, FK_MAX_K);
+    const int kq = k <= 8 ? 8 : k <= 16 ? 16 : k <= 32 ? 32 : 0;  // 0: large-k buffers
 
     // ---- queries -> device operand layout + norms
     const size_t in_row = (size_t)h->d * dtype_bytes(dtype);
@@ -467,135 +611,50 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
       return rc;
     h->nlaunch++;
 
-    // ---- plan
-    int epi = 4;
-    if (const char* e = getenv("FK_EPI")) epi = atoi(e) == 8 ? 8 : 4;
-    const int nh = epi / 4;
-    const int num_m = (int)((nq + BM - 1) / BM);
-    const int n_tiles = (int)((h->ntotal + BN - 1) / BN);
-    int S, chunk_tiles;
-    plan_split(num_m, n_tiles, h->num_sms, 128 / nh, &S, &chunk_tiles);
-    if (const char* e = getenv("FK_FORCE_S")) {
-      S = std::max(1, std::min(atoi(e), std::min(128 / nh, n_tiles)));
-      chunk_tiles = (n_tiles + S - 1) / S;
-      S = (n_tiles + chunk_tiles - 1) / chunk_tiles;
+    Plan pl;
+    if ((rc = make_plan(h, nq, h->ntotal, k, kq, 0, &pl))) return rc;
+    // Large k: estimate each query's bound from a prefix sample -- the exact
+    // 32nd best of m = ntotal*8/k rows sits near the 4k-th overall (it falls
+    // below the true k-th only if >= 32 of the m rows beat it: Poisson(8) >= 32,
+    // p ~ 1e-9 for i.i.d. order).  The merge certifies every query (>= k
+    // survivors under the bound => exact); any failure reruns without it.
+    int64_t m_est = 0;
+    if (kq == 0 && !getenv("FK_NO_EST")) {
+      m_est = ((h->ntotal * 8) / k + BN - 1) / BN * BN;
+      if (m_est < 32 * BN || m_est * 8 > h->ntotal) m_est = 0;
     }
-    const int num_units = num_m * S;
-    const int grid = std::min(num_units, h->num_sms);
-    const int split = split_of(h->storage);
-    const int num_kb = h->dp / chunk_elems_of(h->storage);
-    const int a_bytes = split * num_kb * (int)CHUNK_BYTES;
-    const int a_tmem_cols = h->storage == FK_F32 ? 2 * h->dp : h->dp / 2;
-    int a_mode = a_tmem_cols <= 256 ? 0 : 1;
-    if (const char* e = getenv("FK_FORCE_AMODE")) a_mode = std::max(0, std::min(2, atoi(e)));
-    if (a_mode == 0 && a_tmem_cols > 256) a_mode = 1;
-    const int hist_bytes = kq == 0 ? epi * 1024 : 0;
-    auto stages_for = [&](int mode) {
-      const int avail = SMEM_LIMIT - SMEM_RESERVE - hist_bytes - (mode == 1 ? a_bytes : 0);
-      return avail / ((mode == 2 ? 2 : 1) * split * (int)CHUNK_BYTES);
-    };
-    int stages = stages_for(a_mode);
-    if (a_mode == 1 && stages < 3) {
-      a_mode = 2;
-      stages = stages_for(2);
-    }
-    stages = std::min(stages, 8);
-    if (const char* e = getenv("FK_STAGES")) stages = std::max(2, std::min(stages, atoi(e)));
-    if (stages < 2) return set_err(FK_E_UNSUPPORTED, "pipeline does not fit in shared memory");
-    const int smem = SMEM_RESERVE + hist_bytes + (a_mode == 1 ? a_bytes : 0) +
-                     stages * (a_mode == 2 ? 2 : 1) * split * (int)CHUNK_BYTES;
-    const int S_tot = S * nh;
-
-    if ((rc = h->pkey.ensure((size_t)nq * S_tot * k * sizeof(uint32_t)))) return rc;
-    if ((rc = h->ppos.ensure((size_t)nq * S_tot * k * sizeof(uint32_t)))) return rc;
     if ((rc = h->thr.ensure((size_t)nq * sizeof(uint32_t)))) return rc;
-    CK(cudaMemsetAsync(h->thr.p, 0xFF, (size_t)nq * sizeof(uint32_t), st));
-    int cap = 0;
-    if (kq == 0) {
-      cap = (std::max(2 * k, k + 256) + 31) / 32 * 32;
-      if ((rc = h->pcnt.ensure((size_t)nq * S_tot * sizeof(int)))) return rc;
-      if ((rc = h->cbuf.ensure((size_t)grid * epi * 32 * cap * sizeof(uint64_t)))) return rc;
-    }
-
-    CUtensorMap ta0, ta1, tb0, tb1;
-    const int eb = elem_bytes_of(h->storage);
-    if ((rc = make_map(&ta0, h->q0.p, eb, h->dp, nq))) return rc;
-    if ((rc = make_map(&tb0, h->s0, eb, h->dp, h->ntotal))) return rc;
-    if (h->storage == FK_F32) {
-      if ((rc = make_map(&ta1, h->q1.p, eb, h->dp, nq))) return rc;
-      if ((rc = make_map(&tb1, h->s1, eb, h->dp, h->ntotal))) return rc;
-    } else {
-      ta1 = ta0;
-      tb1 = tb0;
-    }
-    SearchParams sp;
-    sp.qnorm = static_cast<const float*>(h->qn.p);
-    sp.xnorm = h->norms;
-    sp.xn_max = h->xn_max;
-    sp.part_key = static_cast<uint32_t*>(h->pkey.p);
-    sp.part_pos = static_cast<uint32_t*>(h->ppos.p);
-    sp.thr_key = static_cast<uint32_t*>(h->thr.p);
-    sp.part_cnt = static_cast<int*>(h->pcnt.p);
-    sp.cbuf = static_cast<uint64_t*>(h->cbuf.p);
-    sp.cap = cap;
-    sp.dbg_ip = h->dbg_ip;
-    sp.nq = (int)nq;
-    sp.nb = (int)h->ntotal;
-    sp.k = k;
-    sp.num_m = num_m;
-    sp.n_tiles = n_tiles;
-    sp.chunk_tiles = chunk_tiles;
-    sp.S = S;
-    sp.num_units = num_units;
-    sp.num_kb = num_kb;
-    sp.a_mode = a_mode;
-    sp.dbg_flags = 0;
-    if (const char* e = getenv("FK_DEBUG_FLAGS")) sp.dbg_flags = atoi(e);
-    sp.qa0 = h->q0.p;
-    sp.qa1 = h->q1.p;
-    sp.stages = stages;
-    h->plan[0] = grid;
-    h->plan[1] = S;
-    h->plan[2] = chunk_tiles;
-    h->plan[3] = num_units;
-    h->plan[4] = stages;
-    h->plan[5] = a_mode;
-    h->plan[6] = smem;
-    h->plan[7] = kq * 100 + epi;
-
-    if (ev) CK(cudaEventRecord(ev[1], st));
-    if ((rc = launch_fused(epi, h->storage, ip, kq, ta0, ta1, tb0, tb1, sp, grid, smem, st))) return rc;
-    h->nlaunch++;
-    if (ev) CK(cudaEventRecord(ev[2], st));
-
-    if (kq == 0) {
-      int smc = MERGE_SMC;  // FK_MERGE_SMC (tests): lower the smem fast-path limit to exercise the radix fallback
-      if (const char* e = getenv("FK_MERGE_SMC")) smc = std::max(1, std::min(MERGE_SMC, atoi(e)));
-      static bool merge_cfg = false;
-      if (!merge_cfg) {
-        CK(cudaFuncSetAttribute(merge_large_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                MERGE_SMC * 8));
-        CK(cudaFuncSetAttribute(merge_large_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                MERGE_SMC * 8));
-        merge_cfg = true;
+    if ((rc = h->fail.ensure(sizeof(int)))) return rc;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      const bool est = attempt == 0 && m_est > 0;
+      CK(cudaMemsetAsync(h->thr.p, 0xFF, (size_t)nq * sizeof(uint32_t), st));
+      if (ev) CK(cudaEventRecord(ev[1], st));
+      if (est) {
+        Plan pe;
+        if ((rc = make_plan(h, nq, m_est, 32, 32, 1, &pe))) return rc;
+        if ((rc = run_fused(h, pe, nq, m_est, 32, ip, st))) return rc;
+        CK(cudaMemsetAsync(h->fail.p, 0, sizeof(int), st));
       }
-      if (ip)
-        merge_large_kernel<true><<<(unsigned)nq, 256, MERGE_SMC * 8, st>>>(
-            sp.part_key, sp.part_pos, sp.part_cnt, S_tot, (int)nq, k, sp.thr_key, h->ids, dD, dI, dP, smc);
-      else
-        merge_large_kernel<false><<<(unsigned)nq, 256, MERGE_SMC * 8, st>>>(
-            sp.part_key, sp.part_pos, sp.part_cnt, S_tot, (int)nq, k, sp.thr_key, h->ids, dD, dI, dP, smc);
-    } else {
-      const int wpb = 8;
-      const unsigned mgrid = (unsigned)((nq + wpb - 1) / wpb);
-      if (ip)
-        merge_kernel<true><<<mgrid, wpb * 32, 0, st>>>(sp.part_key, sp.part_pos, S_tot, (int)nq, k, h->ids, dD, dI, dP);
-      else
-        merge_kernel<false><<<mgrid, wpb * 32, 0, st>>>(sp.part_key, sp.part_pos, S_tot, (int)nq, k, h->ids, dD, dI, dP);
+      if ((rc = run_fused(h, pl, nq, h->ntotal, k, ip, st))) return rc;
+      if (ev) CK(cudaEventRecord(ev[2], st));
+      if ((rc = launch_merge(h, pl, nq, k, ip, dD, dI, dP, est ? static_cast<int*>(h->fail.p) : nullptr, st)))
+        return rc;
+      if (!est) break;
+      int nfail = 0;
+      CK(cudaMemcpyAsync(&nfail, h->fail.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      h->est_fallbacks += nfail > 0;
+      if (nfail == 0) break;  // every query certified: exact
     }
-    CKL();
-    h->nlaunch++;
     if (ev) CK(cudaEventRecord(ev[3], st));
+    h->plan[0] = pl.grid;
+    h->plan[1] = pl.S;
+    h->plan[2] = pl.chunk_tiles;
+    h->plan[3] = pl.num_units;
+    h->plan[4] = pl.stages;
+    h->plan[5] = pl.a_mode;
+    h->plan[6] = pl.smem;
+    h->plan[7] = kq * 100 + pl.epi;
   }
 
   if (!on_device) {

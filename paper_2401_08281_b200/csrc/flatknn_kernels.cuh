@@ -736,10 +736,80 @@ __global__ void shard_merge_kernel(int nshard, int nq, int k, const float* __res
 }
 
 
+// Block-wide exact k-th smallest (1-based) of n composites read through
+// load(e) (all threads call it; MSB-first 8-bit radix with a shared histogram).
+template <class Load>
+__device__ uint64_t block_kth(Load load, int n, uint32_t k, uint32_t* hist, uint32_t* sel) {
+  const int tid = threadIdx.x;
+  uint64_t prefix = 0;
+  uint32_t need = k;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    const uint64_t hmask = (shift == 56) ? 0ull : (~0ull << (shift + 8));
+    for (int b = tid; b < 256; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    for (int e = tid; e < n; e += blockDim.x) {
+      const uint64_t v = load(e);
+      if ((v & hmask) == prefix) atomicAdd(&hist[static_cast<uint32_t>(v >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (tid < 32) {
+      const int lane = tid;
+      uint32_t c[8], sum = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        c[i] = hist[lane * 8 + i];
+        sum += c[i];
+      }
+      uint32_t incl = sum;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t o = __shfl_up_sync(FULLMASK, incl, off);
+        if (lane >= off) incl += o;
+      }
+      const uint32_t excl = incl - sum;
+      if (excl < need && need <= incl) {
+        uint32_t run = excl;
+        bool done = false;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (!done && run < need && need <= run + c[i]) {
+            sel[0] = lane * 8 + i;
+            sel[1] = run;
+            sel[2] = c[i];
+            done = true;
+          }
+          run += c[i];
+        }
+      }
+    }
+    __syncthreads();
+    const uint32_t bin = sel[0], before = sel[1], bcnt = sel[2];
+    need -= before;
+    prefix |= static_cast<uint64_t>(bin) << shift;
+    __syncthreads();
+    if (bcnt == 1) {
+      const uint64_t m2 = ~0ull << shift;
+      for (int e = tid; e < n; e += blockDim.x) {
+        const uint64_t v = load(e);
+        if ((v & m2) == prefix) {
+          sel[3] = static_cast<uint32_t>(v >> 32);
+          sel[4] = static_cast<uint32_t>(v);
+        }
+      }
+      __syncthreads();
+      const uint64_t r = (static_cast<uint64_t>(sel[3]) << 32) | sel[4];
+      __syncthreads();
+      return r;
+    }
+  }
+  return prefix;
+}
+
 // Large-k final merge: one CTA per query.  Survivors of every partial list
-// with key <= the query's final shared bound (>= k of them, and a superset of
-// the true top-k) are gathered into smem and bitonic-sorted by (key, position);
-// if they do not fit, an exact radix select over the lists picks the k-th first.
+// with key <= the query's final shared bound (a superset of the true top-k,
+// at least k of them) are gathered into smem; an exact block radix select
+// finds the k-th (key, position); the k winners are bitonic-sorted.  If the
+// survivors overflow smem the select reads the lists from global instead.
 template <bool IS_IP>
 __global__ void __launch_bounds__(256) merge_large_kernel(const uint32_t* __restrict__ pkey,
                                                           const uint32_t* __restrict__ ppos,
@@ -747,11 +817,10 @@ __global__ void __launch_bounds__(256) merge_large_kernel(const uint32_t* __rest
                                                           const uint32_t* __restrict__ thr_key,
                                                           const int64_t* __restrict__ ids, float* __restrict__ D,
                                                           int64_t* __restrict__ I, int64_t* __restrict__ P,
-                                                          int smc) {
-  extern __shared__ uint64_t sm[];
-  __shared__ int count;
-  __shared__ uint32_t hist[256];
-  __shared__ uint64_t kth_s;
+                                                          int smc, int* __restrict__ fail) {
+  extern __shared__ uint64_t sm[];  // smc survivors, then the k winners (pow2-padded)
+  __shared__ int count, count2;
+  __shared__ uint32_t hist[256], sel[8];
   const int q = blockIdx.x;
   const int tid = threadIdx.x;
   if (q >= nq) return;
@@ -759,45 +828,60 @@ __global__ void __launch_bounds__(256) merge_large_kernel(const uint32_t* __rest
   const uint32_t* lk = pkey + (size_t)q * S * k;
   const uint32_t* lp = ppos + (size_t)q * S * k;
   const int* lc = pcnt + (size_t)q * S;
-  if (tid == 0) count = 0;
+  if (tid == 0) {
+    count = 0;
+    count2 = 0;
+  }
   __syncthreads();
   const int total = S * k;
-  auto load = [&](int e) -> uint64_t {
+  auto gload = [&](int e) -> uint64_t {
     const int s = e / k, i = e - s * k;
     if (i >= lc[s]) return ~0ull;
     const uint32_t key = lk[e];
     if (key > thr) return ~0ull;
     return (static_cast<uint64_t>(key) << 32) | lp[e];
   };
-  for (int e = tid; e < total; e += blockDim.x) {
-    const uint64_t v = load(e);
-    if (v != ~0ull) {
-      const int idx = atomicAdd(&count, 1);
-      if (idx < smc) sm[idx] = v;
+  for (int s = tid >> 5; s < S; s += blockDim.x >> 5) {  // warp per list: coalesced
+    const int c = lc[s];
+    for (int i = tid & 31; i < c; i += 32) {
+      const uint32_t key = lk[(size_t)s * k + i];
+      if (key <= thr) {
+        const int idx = atomicAdd(&count, 1);
+        if (idx < smc) sm[idx] = (static_cast<uint64_t>(key) << 32) | lp[(size_t)s * k + i];
+      }
     }
   }
   __syncthreads();
-  int n = count;
-  if (n > smc) {  // rare (massive exact ties): exact k-th first, then gather exactly k
-    if (tid < 32) {
-      const uint64_t kth = warp_kth(load, total, (uint32_t)min(k, n), hist);
-      if (tid == 0) {
-        kth_s = kth;
-        count = 0;
+  const int n = count;
+  // certification (estimated bound): fewer than k survivors means the bound
+  // may have excluded true neighbours -> the host reruns without the estimate
+  if (fail != nullptr && n < k && tid == 0) atomicAdd(fail, 1);
+  uint64_t* win = sm + smc;  // k winners
+  int nw;
+  if (n <= k) {
+    for (int i = tid; i < n; i += blockDim.x) win[i] = sm[i];
+    nw = n;
+  } else {
+    uint64_t kth;
+    if (n <= smc)
+      kth = block_kth([&](int e) { return sm[e]; }, n, (uint32_t)k, hist, sel);
+    else
+      kth = block_kth(gload, total, (uint32_t)k, hist, sel);
+    if (n <= smc) {
+      for (int i = tid; i < n; i += blockDim.x)
+        if (sm[i] <= kth) win[atomicAdd(&count2, 1)] = sm[i];
+    } else {
+      for (int e = tid; e < total; e += blockDim.x) {
+        const uint64_t v = gload(e);
+        if (v != ~0ull && v <= kth) win[atomicAdd(&count2, 1)] = v;
       }
     }
     __syncthreads();
-    const uint64_t kth = kth_s;
-    for (int e = tid; e < total; e += blockDim.x) {
-      const uint64_t v = load(e);
-      if (v != ~0ull && v <= kth) sm[atomicAdd(&count, 1)] = v;
-    }
-    __syncthreads();
-    n = count;
+    nw = count2;  // == k (composites are unique)
   }
   int P2 = 1;
-  while (P2 < n) P2 <<= 1;
-  for (int i = n + tid; i < P2; i += blockDim.x) sm[i] = ~0ull;
+  while (P2 < nw) P2 <<= 1;
+  for (int i = nw + tid; i < P2; i += blockDim.x) win[i] = ~0ull;
   __syncthreads();
   for (int size = 2; size <= P2; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
@@ -805,10 +889,10 @@ __global__ void __launch_bounds__(256) merge_large_kernel(const uint32_t* __rest
         const int lo = 2 * i - (i & (stride - 1));
         const int hi = lo + stride;
         const bool asc = (lo & size) == 0;
-        const uint64_t a = sm[lo], b = sm[hi];
+        const uint64_t a = win[lo], b = win[hi];
         if ((a > b) == asc) {
-          sm[lo] = b;
-          sm[hi] = a;
+          win[lo] = b;
+          win[hi] = a;
         }
       }
       __syncthreads();
@@ -816,7 +900,7 @@ __global__ void __launch_bounds__(256) merge_large_kernel(const uint32_t* __rest
   }
   for (int r = tid; r < k; r += blockDim.x) {
     const size_t o = (size_t)q * k + r;
-    const uint64_t w = r < n ? sm[r] : ~0ull;
+    const uint64_t w = r < nw ? win[r] : ~0ull;
     if (w == ~0ull) {
       D[o] = IS_IP ? -INFINITY : INFINITY;
       I[o] = -1;

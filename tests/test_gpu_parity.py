@@ -299,3 +299,38 @@ def test_k_above_max_rejected():
     idx.add(np.zeros((10, 4), np.float32))
     with pytest.raises(NotImplementedError):
         idx.search(np.zeros((1, 4), np.float32), 4096)
+
+
+@pytest.mark.parametrize("k,metric", [(100, "l2"), (1024, "ip")])
+def test_large_k_estimated_bound_path(k, metric):
+    """nb large enough that the prefix-sample bound estimate is used."""
+    rng = np.random.default_rng(k)
+    xb = rng.standard_normal((300_000, 32), dtype=np.float32)
+    q = rng.standard_normal((130, 32), dtype=np.float32)
+    idx = FlatIndex(32, METRIC_L2 if metric == "l2" else METRIC_IP)
+    idx.add(xb)
+    res = idx.search(q, k)
+    os.environ["FK_NO_EST"] = "1"
+    try:
+        ref = idx.search(q, k)
+    finally:
+        del os.environ["FK_NO_EST"]
+    assert np.array_equal(res.ids, ref.ids) and np.array_equal(res.distances, ref.distances)
+    sub = np.arange(0, 130, 13)
+    want_ids, want_dist = O.flat_search_blas(xb, q[sub], k, metric)
+    assert_parity(res.ids[sub], res.distances[sub], want_ids, want_dist)
+
+
+def test_large_k_estimate_fails_certification_and_reruns():
+    """Adversarial order: the prefix sample holds all near neighbours, so the
+    estimated bound is too tight (< k survivors) -> exact rerun must kick in."""
+    rng = np.random.default_rng(3)
+    near = rng.standard_normal((40_000, 16), dtype=np.float32) * 0.01
+    far = rng.standard_normal((260_000, 16), dtype=np.float32) + 50.0
+    xb = np.vstack([near, far])
+    q = rng.standard_normal((64, 16), dtype=np.float32) * 0.01
+    idx = IndexFlatL2(16)
+    idx.add(xb)
+    res = idx.search(q, 200)
+    want_ids, want_dist = O.flat_search_blas(xb, q, 200, "l2")
+    assert_parity(res.ids, res.distances, want_ids, want_dist)
