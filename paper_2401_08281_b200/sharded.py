@@ -15,8 +15,6 @@ result on the same data.
 
 from __future__ import annotations
 
-import ctypes
-
 import numpy as np
 
 from .core import METRIC_L2, Metric, SearchResult, as_vectors, is_torch, metric_value
@@ -107,6 +105,17 @@ class ShardedFlatIndex:
         shard, e.g. the 100M-row config).  Collective: every rank calls it."""
         x_local = as_vectors(x_local, self.d)
         self._add_local(x_local, self.ntotal + global_offset, ids=ids_local)
+        self.ntotal += int(n_global)
+
+    def add_shard_rows(self, x_rows, global_row0: int) -> None:
+        """Append rows of this rank's shard whose positions in the global batch
+        being built start at ``global_row0`` (relative to ntotal before the
+        batch).  Call ``finish_global_batch(n_global)`` once on every rank when
+        all ranks have added their rows (bulk loads generated in pieces)."""
+        x_rows = as_vectors(x_rows, self.d)
+        self._add_local(x_rows, self.ntotal + global_row0, ids=None)
+
+    def finish_global_batch(self, n_global: int) -> None:
         self.ntotal += int(n_global)
 
     def _add_local(self, xs, gpos0: int, ids) -> None:

@@ -1,0 +1,11 @@
+#!/bin/bash
+# Official evidence pass: bench line (N=1), ncu launch list of the bench command,
+# one ncu --set full capture of the fused kernel, SASS listing.
+mkdir -p gpurun_out
+TAG=${TAG:-r01}
+timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err; echo "bench rc=$?"
+tail -1 gpurun_out/bench_${TAG}.json | cut -c1-400
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_${TAG}.csv \
+   python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/launches_bench_${TAG}.log 2>&1; echo "launches rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:fused_knn -s 2 -c 1 \
+   -o gpurun_out/full_${TAG} -f python scripts/prof_search.py --config 2 --iters 3 > gpurun_out/ncu_full_${TAG}.log 2>&1; echo "ncu full rc=$?"

@@ -5,7 +5,7 @@ import time
 import json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
-from bench import CONFIGS, gen_base, gen_queries
+from bench import CONFIGS, gen_base, gen_base_device, gen_queries
 from paper_2401_08281_b200 import FlatIndex, METRIC_L2, METRIC_IP
 
 cfgn = int(os.environ.get("CFG", "2"))
@@ -16,7 +16,9 @@ for kv in os.environ.get("OVERRIDE", "").split(","):
         cfg[a] = int(b) if b.isdigit() else b
 idx = FlatIndex(cfg["d"], METRIC_L2 if cfg["metric"] == "l2" else METRIC_IP, storage=cfg["storage"])
 for lo in range(0, cfg["nb"], 2_000_000):
-    idx.add(torch.from_numpy(gen_base(cfg, lo, min(cfg["nb"], lo + 2_000_000))).cuda())
+    hi = min(cfg["nb"], lo + 2_000_000)
+    idx.add(torch.from_numpy(gen_base(cfg, lo, hi)).cuda() if cfg["nb"] <= 2_000_000 else gen_base_device(cfg, lo, hi))
+    torch.cuda.empty_cache()
 q = torch.from_numpy(gen_queries(cfg)).cuda()
 variants = [v for v in sys.argv[1:]] or [""]
 ref = None
