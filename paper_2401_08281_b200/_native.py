@@ -53,6 +53,7 @@ _SIGS = {
     "fk_kernel_times": (_INT, [_P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(_INT)]),
     "fk_last_plan": (_INT, [_P, ctypes.POINTER(_INT)]),
     "fk_debug_set_ip_dump": (_INT, [_P, _P]),
+    "fk_debug_set_trace": (_INT, [_P, _P]),
 }
 
 

@@ -91,7 +91,7 @@ int make_map(CUtensorMap* m, const void* base, int elem_bytes, uint64_t cols, ui
 constexpr int FK_MAX_K = 2048;
 constexpr int MERGE_SMC = 16384;    // large-k merge: survivors gathered in smem (128 KB) + 2048 winners
 constexpr int SMEM_LIMIT = 232448;  // sm_100 max dynamic smem per block (227 KB)
-constexpr int SMEM_RESERVE = 1024 /*align*/ + 2 * BN * 4 /*norm tiles*/ + 256 /*barriers + tmem slot*/;
+constexpr int SMEM_RESERVE = 1024 /*align*/ + 512 /*barriers + tmem slot*/;
 
 int elem_bytes_of(int storage) { return storage == FK_F32 ? 4 : 2; }
 int chunk_elems_of(int storage) { return storage == FK_F32 ? 32 : 64; }
@@ -142,6 +142,7 @@ struct fk_index {
   long long nlaunch_acc = 0;  // launches since the last fk_kernel_times
   int plan[8] = {0};
   float* dbg_ip = nullptr;  // test hook (FK_DEBUG_IP)
+  unsigned long long* trace = nullptr;  // debug timeline hook
 };
 
 namespace {
@@ -409,7 +410,7 @@ int fk_add(fk_index* h, const void* x, int64_t n, int dtype, const int64_t* ids,
 namespace {
 
 struct Plan {
-  int kq, epi, nh, num_m, n_tiles, S, chunk_tiles, num_units, grid, a_mode, stages, smem, S_tot, cap;
+  int kq, epi, nh, num_m, n_tiles, S, chunk_tiles, num_units, grid, a_mode, stages, smem, S_tot, cap, xn_slots;
 };
 
 // Tile / split-N / pipeline plan for one fused pass over base rows [0, nb_pass).
@@ -439,8 +440,11 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   if (const char* e = getenv("FK_FORCE_AMODE")) P.a_mode = std::max(0, std::min(2, atoi(e)));
   if (P.a_mode == 0 && a_tmem_cols > 256) P.a_mode = 1;
   const int hist_bytes = kq == 0 ? P.epi * 1024 : 0;
+  // norm-tile ring: 3 slots when smem is tight (fp32), 8 otherwise
+  P.xn_slots = (h->storage == FK_F32 && P.a_mode != 2) ? 3 : 8;
+  const int xn_bytes = P.xn_slots * BN * 4;
   auto stages_for = [&](int mode) {
-    const int avail = SMEM_LIMIT - SMEM_RESERVE - hist_bytes - (mode == 1 ? a_bytes : 0);
+    const int avail = SMEM_LIMIT - SMEM_RESERVE - hist_bytes - xn_bytes - (mode == 1 ? a_bytes : 0);
     return avail / ((mode == 2 ? 2 : 1) * split * (int)CHUNK_BYTES);
   };
   P.stages = stages_for(P.a_mode);
@@ -451,7 +455,7 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   P.stages = std::min(P.stages, 8);
   if (const char* e = getenv("FK_STAGES")) P.stages = std::max(2, std::min(P.stages, atoi(e)));
   if (P.stages < 2) return set_err(FK_E_UNSUPPORTED, "pipeline does not fit in shared memory");
-  P.smem = SMEM_RESERVE + hist_bytes + (P.a_mode == 1 ? a_bytes : 0) +
+  P.smem = SMEM_RESERVE + hist_bytes + xn_bytes + (P.a_mode == 1 ? a_bytes : 0) +
            P.stages * (P.a_mode == 2 ? 2 : 1) * split * (int)CHUNK_BYTES;
   P.S_tot = P.S * P.nh;
   P.cap = kq == 0 ? (std::max(2 * k, k + 256) + 31) / 32 * 32 : 0;
@@ -492,6 +496,7 @@ int run_fused(fk_index* h, const Plan& P, int64_t nq, int64_t nb_pass, int k, bo
   sp.cbuf = static_cast<uint64_t*>(h->cbuf.p);
   sp.cap = P.cap;
   sp.dbg_ip = h->dbg_ip;
+  sp.trace = h->trace;
   sp.qa0 = h->q0.p;
   sp.qa1 = h->q1.p;
   sp.nq = (int)nq;
@@ -505,6 +510,9 @@ int run_fused(fk_index* h, const Plan& P, int64_t nq, int64_t nb_pass, int k, bo
   sp.num_kb = h->dp / chunk_elems_of(h->storage);
   sp.a_mode = P.a_mode;
   sp.stages = P.stages;
+  sp.xn_slots = P.xn_slots;
+  sp.n_issuers = P.stages >= 4 ? 2 : 1;  // each issuer needs a sub-ring of >= 2 slots
+  if (const char* e = getenv("FK_ISSUERS")) sp.n_issuers = (atoi(e) == 1 || P.stages < 4) ? 1 : 2;
   if (const char* e = getenv("FK_DEBUG_FLAGS")) sp.dbg_flags = atoi(e);
   rc = launch_fused(P.epi, h->storage, ip, P.kq, ta0, ta1, tb0, tb1, sp, P.grid, P.smem, st);
   if (rc == FK_OK) h->nlaunch++;
@@ -804,6 +812,12 @@ int fk_last_plan(fk_index* h, int* out8) {
 
 // Test hook (not in the public header): route raw inner products of the next
 // searches to a caller-owned device buffer [nq][ntotal] (NULL disables).
+int fk_debug_set_trace(fk_index* h, unsigned long long* dev_buf) {
+  if (!h) return set_err(FK_E_INVALID, "NULL index");
+  h->trace = dev_buf;
+  return FK_OK;
+}
+
 int fk_debug_set_ip_dump(fk_index* h, float* dev_buf) {
   if (!h) return set_err(FK_E_INVALID, "NULL index");
   h->dbg_ip = dev_buf;

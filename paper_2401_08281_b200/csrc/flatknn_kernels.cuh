@@ -57,6 +57,9 @@ struct SearchParams {
   int num_kb;      // padded d / elements-per-128B-chunk
   int a_mode;      // 0: queries in TMEM, 1: resident in smem, 2: streamed per stage
   int stages;      // B (and streamed A) pipeline depth
+  int xn_slots;    // base-norm tile ring depth (prefetched by the producer)
+  unsigned long long* trace;  // debug timeline (CTA 0): [tile][16] clock64 stamps
+  int n_issuers;   // MMA-issuing threads (warps 1 and 3)
   int dbg_flags;   // bottleneck experiments: 1 = epilogue skips compute, 2 = producer skips TMA
 };
 
@@ -255,17 +258,19 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
 
   uint8_t* a_region = smem;
   uint8_t* st_region = smem + a_bytes;
-  float* xn_s = reinterpret_cast<float*>(st_region + stages * stage_bytes);  // [2][BN]
-  uint32_t* hist_base = reinterpret_cast<uint32_t*>(xn_s + 2 * BN);  // large-k: [EPI][256]
+  const int xn_slots = p.xn_slots;
+  float* xn_s = reinterpret_cast<float*>(st_region + stages * stage_bytes);  // [xn_slots][BN]
+  uint32_t* hist_base = reinterpret_cast<uint32_t*>(xn_s + xn_slots * BN);  // large-k: [EPI][256]
   uint64_t* bars = reinterpret_cast<uint64_t*>(hist_base + (KQ == 0 ? EPI * 256 : 0));
-  uint64_t* full = bars;
-  uint64_t* empty = bars + stages;
-  uint64_t* tfull = bars + 2 * stages;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* xfull = tempty + 2;
-  uint64_t* afull = xfull + 2;
-  uint64_t* aempty = afull + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 1);
+  uint64_t* full = bars;         // [8]
+  uint64_t* empty = bars + 8;    // [8]
+  uint64_t* tfull = bars + 16;   // [2]
+  uint64_t* tempty = bars + 18;  // [2]
+  uint64_t* xfull = bars + 20;   // [8]
+  uint64_t* xempty = bars + 28;  // [8]
+  uint64_t* afull = bars + 36;
+  uint64_t* aempty = bars + 37;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 38);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_b0);
@@ -283,10 +288,13 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], EPI);
-      mbar_init(&xfull[b], 1);
+    }
+    for (int x = 0; x < xn_slots; ++x) {
+      mbar_init(&xfull[x], 1);
+      mbar_init(&xempty[x], EPI);
     }
     mbar_init(afull, a_mode == 0 ? EPI : 1);
-    mbar_init(aempty, 1);
+    mbar_init(aempty, p.n_issuers);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, tmem_cols);
@@ -300,7 +308,11 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     if (lane == 0) {
       const uint64_t pol_a = policy_evict_last();
       const uint64_t pol_b = policy_evict_first();
-      uint32_t stage = 0, phase = 0;
+      // one FIFO sub-ring of `sh` slots per MMA issuer (tile t -> ring t % nis)
+      const uint32_t nis = p.n_issuers;
+      const uint32_t sh = (uint32_t)stages / nis;
+      uint32_t rs[2] = {0, 0}, rph[2] = {0, 0};
+      uint32_t xt = 0, tc = 0;
       int j = 0;
       for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++j) {
         const int chunk = u / p.num_m;
@@ -315,15 +327,24 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
               tma_load_2d(a_region + (part * num_kb + kb) * CHUNK_BYTES, part ? &tm_a1 : &tm_a0, afull,
                           kb * BK, m * BM, pol_a);
         }
-        for (int t = t0; t < t1; ++t) {
+        for (int t = t0; t < t1; ++t, ++tc) {
+          const uint32_t ring = tc % nis;
+          if (!IS_IP) {  // base norms of this tile -> ring slot (consumed by the epilogue)
+            const uint32_t xs = xt % xn_slots, xph = (xt / xn_slots) & 1;
+            mbar_wait(&xempty[xs], xph ^ 1);
+            mbar_arrive_expect_tx(&xfull[xs], BN * sizeof(float));
+            bulk_load(xn_s + xs * BN, p.xnorm + (size_t)t * BN, BN * sizeof(float), &xfull[xs]);
+            ++xt;
+          }
           for (int kb = 0; kb < num_kb; ++kb) {
+            const uint32_t stage = ring * sh + rs[ring], phase = rph[ring];
+            if (++rs[ring] == sh) {
+              rs[ring] = 0;
+              rph[ring] ^= 1;
+            }
             mbar_wait(&empty[stage], phase ^ 1);
             if (p.dbg_flags & 2) {  // experiment: no data movement
               mbar_arrive(&full[stage]);
-              if (++stage == (uint32_t)stages) {
-                stage = 0;
-                phase ^= 1;
-              }
               continue;
             }
             mbar_arrive_expect_tx(&full[stage], stage_bytes);
@@ -335,18 +356,21 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
               if (SPLIT == 2)
                 tma_load_2d(sb + 3 * CHUNK_BYTES, &tm_a1, &full[stage], kb * BK, m * BM, pol_a);
             }
-            if (++stage == (uint32_t)stages) {
-              stage = 0;
-              phase ^= 1;
-            }
           }
         }
       }
     }
-  } else if (warp == 1) {
-    // ===================== MMA issuer (single thread) =====================
+  } else if (warp == 1 || (warp == 3 && p.n_issuers == 2)) {
+    // ===================== MMA issuers (one thread each) =====================
+    // With two issuers (warps 1 and 3), issuer w owns the tiles with
+    // tcount % 2 == w and hence accumulator buffer w: while one waits on its
+    // barriers the other keeps the tensor pipe fed.
     if (lane == 0) {
-      uint32_t stage = 0, phase = 0, tcount = 0;
+      const uint32_t nis = p.n_issuers;
+      const uint32_t mw = (warp == 1) ? 0u : 1u;
+      const uint32_t sh = (uint32_t)stages / nis;
+      uint32_t rslot = 0, rphase = 0;  // position in this issuer's sub-ring
+      uint32_t tcount = 0;
       int j = 0;
       const uint32_t a_tm = tmem_base + TMEM_A_COL;
       const uint32_t a_lo_off = (MODE == 0) ? (uint32_t)(num_kb * 32) : 0u;  // lo half after hi (columns)
@@ -359,17 +383,23 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
           tc_fence_after();
         }
         for (int t = t0; t < t1; ++t, ++tcount) {
+          if (tcount % nis != mw) continue;
           const uint32_t buf = tcount & 1, tph = (tcount >> 1) & 1;
+          const bool tr = p.trace != nullptr && blockIdx.x == 0 && tcount < 256;
+          if (tr) p.trace[tcount * 16 + 0] = clock64();
           mbar_wait(&tempty[buf], tph ^ 1);
           tc_fence_after();
-          if (!IS_IP) {
-            mbar_arrive_expect_tx(&xfull[buf], BN * sizeof(float));
-            bulk_load(xn_s + buf * BN, p.xnorm + (size_t)t * BN, BN * sizeof(float), &xfull[buf]);
-          }
+          if (tr) p.trace[tcount * 16 + 1] = clock64();
           const uint32_t d_tmem = tmem_base + buf * BN;
           for (int kb = 0; kb < num_kb; ++kb) {
+            const uint32_t stage = mw * sh + rslot, phase = rphase;
+            if (++rslot == sh) {
+              rslot = 0;
+              rphase ^= 1;
+            }
             mbar_wait(&full[stage], phase);
             tc_fence_after();
+            if (tr && kb < 4) p.trace[tcount * 16 + 13 + (kb < 3 ? kb : 2)] = clock64();
             uint8_t* sb = st_region + stage * stage_bytes;
             const uint64_t bd0 = smem_desc_sw128(smem_u32(sb));
             if (a_mode == 0) {
@@ -408,12 +438,10 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
               }
             }
             mma_commit(&empty[stage]);
-            if (++stage == (uint32_t)stages) {
-              stage = 0;
-              phase ^= 1;
-            }
+            if (tr && kb < 4) p.trace[tcount * 16 + 9 + kb] = clock64();
           }
           mma_commit(&tfull[buf]);
+          if (tr) p.trace[tcount * 16 + 3] = clock64();
         }
         if (a_mode == 1) mma_commit(aempty);
       }
@@ -519,12 +547,17 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
 
       for (int t = t0; t < t1; ++t, ++tcount) {
         const uint32_t buf = tcount & 1, tph = (tcount >> 1) & 1;
+        const uint32_t xslot = tcount % xn_slots, xph = (tcount / xn_slots) & 1;
+        const bool tr = p.trace != nullptr && blockIdx.x == 0 && tcount < 256 && ew == 0 && lane == 0;
+        if (tr) p.trace[tcount * 16 + 4] = clock64();
         mbar_wait(&tfull[buf], tph);
-        if (!IS_IP) mbar_wait(&xfull[buf], tph);
+        if (tr) p.trace[tcount * 16 + 5] = clock64();
+        if (!IS_IP) mbar_wait(&xfull[xslot], xph);
         tc_fence_after();
+        if (tr) p.trace[tcount * 16 + 6] = clock64();
         const int n0 = t * BN + h * COLS;
         const int nvalid = p.nb - n0;
-        const float* xs = xn_s + buf * BN + h * COLS;
+        const float* xs = xn_s + xslot * BN + h * COLS;
         // Filter on f = xn - 2 ip (L2; one FMA) or -ip (IP) against T; the
         // exact reference value (qn + xn) - 2 ip is computed for survivors only.
         auto process = [&](const uint32_t (&r)[32], int c0) {
@@ -592,7 +625,11 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[buf]);
+        if (tr) p.trace[tcount * 16 + 7] = clock64();
+        if (lane == 0) {
+          mbar_arrive(&tempty[buf]);
+          if (!IS_IP) mbar_arrive(&xempty[xslot]);
+        }
         if (((t - t0) & 15) == 15 && row_ok) {  // publish own k-th, fetch the shared bound
           const uint32_t mine = own_key();
           gkey = min(atomicMin(p.thr_key + row, mine), mine);

@@ -1,0 +1,33 @@
+"""Per-tile clock64 timeline of CTA 0 (producer/MMA/epilogue handoffs)."""
+import ctypes, os, sys, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+from bench import CONFIGS, gen_base, gen_queries
+from paper_2401_08281_b200 import FlatIndex, METRIC_L2, METRIC_IP
+from paper_2401_08281_b200 import _native as N
+cfg = dict(CONFIGS[int(os.environ.get("CFG", "2"))])
+for kv in os.environ.get("OVERRIDE", "").split(","):
+    if kv:
+        a, b = kv.split("="); cfg[a] = int(b) if b.isdigit() else b
+nb = min(cfg["nb"], 2_000_000)
+idx = FlatIndex(cfg["d"], METRIC_L2 if cfg["metric"] == "l2" else METRIC_IP, storage=cfg["storage"])
+idx.add(torch.from_numpy(gen_base(dict(cfg, nb=nb))).cuda())
+q = torch.from_numpy(gen_queries(cfg)).cuda()
+idx.search(q, cfg["k"]); torch.cuda.synchronize()
+buf = torch.zeros(256 * 16, dtype=torch.int64, device="cuda")
+N.check(N.lib().fk_debug_set_trace(idx._h, ctypes.c_void_p(buf.data_ptr())))
+idx.search(q, cfg["k"]); torch.cuda.synchronize()
+N.check(N.lib().fk_debug_set_trace(idx._h, None))
+t = buf.cpu().numpy().reshape(256, 16).astype(np.int64)
+t0 = t[0, 0]
+print("plan", idx.last_plan(), os.environ.get("FK_DEBUG_FLAGS"))
+for i in list(range(100, 106)):
+    r = t[i] - t0
+    print(i, f"wait_tempty {r[0]} got {r[1]} | kb0 full {r[13]} kb0 issued {r[9]} | kb1 full {r[14]} kb1 issued {r[10]} | commit {r[3]} || epi wait {r[4]} got {r[5]} done {r[7]}")
+sl = slice(20, 240)
+print("period", np.median(np.diff(t[sl, 3])))
+print("mma wait tempty", np.median(t[sl, 1] - t[sl, 0]), "| got_tempty->kb0 full", np.median(t[sl, 13] - t[sl, 1]),
+      "| kb0 full->kb0 issued", np.median(t[sl, 9] - t[sl, 13]), "| kb0 issued->kb1 full", np.median(t[sl, 14] - t[sl, 9]),
+      "| kb1 full->issued", np.median(t[sl, 10] - t[sl, 14]))
+print("epi: commit->got_tfull", np.median(t[sl, 5] - t[sl, 3]), "| busy", np.median(t[sl, 7] - t[sl, 6]),
+      "| epi done -> mma got tempty(next use)", np.median(t[22:242, 1] - t[20:240, 7]))
