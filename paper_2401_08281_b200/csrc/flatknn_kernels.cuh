@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       // one FIFO sub-ring of `sh` slots per MMA issuer (tile t -> ring t % nis)
       const uint32_t nis = p.n_issuers;
       const uint32_t sh = (uint32_t)stages / nis;
-      uint32_t rs[2] = {0, 0}, rph[2] = {0, 0};
+      uint32_t rs0 = 0, rph0 = 0, rs1 = 0, rph1 = 0;  // sub-ring positions (scalars: no local memory)
       uint32_t xt = 0, tc = 0;
       int j = 0;
       for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++j) {
@@ -337,10 +337,12 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             ++xt;
           }
           for (int kb = 0; kb < num_kb; ++kb) {
-            const uint32_t stage = ring * sh + rs[ring], phase = rph[ring];
-            if (++rs[ring] == sh) {
-              rs[ring] = 0;
-              rph[ring] ^= 1;
+            uint32_t& rs = ring ? rs1 : rs0;
+            uint32_t& rph = ring ? rph1 : rph0;
+            const uint32_t stage = ring * sh + rs, phase = rph;
+            if (++rs == sh) {
+              rs = 0;
+              rph ^= 1;
             }
             mbar_wait(&empty[stage], phase ^ 1);
             if (p.dbg_flags & 2) {  // experiment: no data movement
@@ -568,10 +570,9 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(r[j]);
             m = -reduce32<true>(f);  // min(-ip) = -max(ip)
           } else {
-            const float4* xs4 = reinterpret_cast<const float4*>(xs + c0);
 #pragma unroll
             for (int j4 = 0; j4 < 8; ++j4) {
-              const float4 x = xs4[j4];
+              const float4 x = lds_f4(xs + c0 + 4 * j4);
               f[4 * j4 + 0] = fmaf(-2.f, __uint_as_float(r[4 * j4 + 0]), x.x);
               f[4 * j4 + 1] = fmaf(-2.f, __uint_as_float(r[4 * j4 + 1]), x.y);
               f[4 * j4 + 2] = fmaf(-2.f, __uint_as_float(r[4 * j4 + 2]), x.z);
@@ -591,7 +592,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
               cand &= cand - 1;
               const float ip = select32(reinterpret_cast<const float(&)[32]>(r), j);
               // flat.py:111: dmat = (qn + norms) - 2.0*ip  (2*ip exact -> one FMA)
-              float v = IS_IP ? -ip : fmaf(-2.f, ip, qn + xs[c0 + j]);
+              float v = IS_IP ? -ip : fmaf(-2.f, ip, qn + lds_f32(xs + c0 + j));
               if (!(v > thr)) {
                 if (!IS_IP) v = (v <= 0.f) ? 0.f : v;  // np.maximum(dmat, 0) (flat.py:112)
                 if constexpr (KQ > 0) {
@@ -605,31 +606,37 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             }
           }
         };
-#pragma unroll 1
-        for (int c = 0; c < ((p.dbg_flags & 1) ? 0 : COLS / 64); ++c) {
-          uint32_t ra[32], rb[32];
-          const uint32_t ta = tmem_base + lane_addr + buf * BN + h * COLS + c * 64;
-          tmem_ld_32x32b_x32(ta, ra);
-          tmem_ld_32x32b_x32(ta + 32, rb);
+        // (1) pull this warp's accumulator slice into registers, (2) hand the
+        // TMEM buffer straight back to the MMA issuer, (3) filter + select from
+        // registers while the tensor pipe already fills the buffer again.
+        const bool do_epi = !(p.dbg_flags & 1);
+        uint32_t racc[COLS];
+        if (do_epi) {
+#pragma unroll
+          for (int c = 0; c < COLS / 32; ++c)
+            tmem_ld_32x32b_x32(tmem_base + lane_addr + buf * BN + h * COLS + c * 32,
+                               *reinterpret_cast<uint32_t(*)[32]>(&racc[32 * c]));
           tmem_ld_wait();
-          if (p.dbg_ip != nullptr && row_ok) {
-            for (int j = 0; j < 32; ++j) {
-              if (c * 64 + j < nvalid) p.dbg_ip[(size_t)row * p.nb + n0 + c * 64 + j] = __uint_as_float(ra[j]);
-              if (c * 64 + 32 + j < nvalid)
-                p.dbg_ip[(size_t)row * p.nb + n0 + c * 64 + 32 + j] = __uint_as_float(rb[j]);
-            }
-          }
-          process(ra, c * 64);
-          process(rb, c * 64 + 32);
-          if constexpr (KQ == 0) compact_lanes(p.cap - 64);  // room for the next 64 columns
         }
         tc_fence_before();
         __syncwarp();
-        if (tr) p.trace[tcount * 16 + 7] = clock64();
-        if (lane == 0) {
-          mbar_arrive(&tempty[buf]);
-          if (!IS_IP) mbar_arrive(&xempty[xslot]);
+        if (lane == 0) mbar_arrive(&tempty[buf]);
+        if (do_epi) {
+          if (p.dbg_ip != nullptr && row_ok) {
+            for (int j = 0; j < COLS; ++j)
+              if (j < nvalid) p.dbg_ip[(size_t)row * p.nb + n0 + j] = __uint_as_float(racc[j]);
+          }
+#pragma unroll
+          for (int c = 0; c < COLS / 32; ++c) {
+            process(*reinterpret_cast<const uint32_t(*)[32]>(&racc[32 * c]), c * 32);
+            if constexpr (KQ == 0) {
+              if (c & 1) compact_lanes(p.cap - 64);  // room for the next 64 columns
+            }
+          }
         }
+        __syncwarp();
+        if (tr) p.trace[tcount * 16 + 7] = clock64();
+        if (lane == 0 && !IS_IP) mbar_arrive(&xempty[xslot]);
         if (((t - t0) & 15) == 15 && row_ok) {  // publish own k-th, fetch the shared bound
           const uint32_t mine = own_key();
           gkey = min(atomicMin(p.thr_key + row, mine), mine);
