@@ -458,7 +458,7 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   P.smem = SMEM_RESERVE + hist_bytes + xn_bytes + (P.a_mode == 1 ? a_bytes : 0) +
            P.stages * (P.a_mode == 2 ? 2 : 1) * split * (int)CHUNK_BYTES;
   P.S_tot = P.S * P.nh;
-  P.cap = kq == 0 ? (std::max(2 * k, k + 256) + 31) / 32 * 32 : 0;
+  P.cap = kq == 0 ? (std::max(2 * k, k + 256) + 31) / 32 * 32 : 0;  // >= k + one tile (128) of slack
   *pl = P;
   return FK_OK;
 }

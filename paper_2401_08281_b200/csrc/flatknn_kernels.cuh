@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       const uint32_t nis = p.n_issuers;
       const uint32_t sh = (uint32_t)stages / nis;
       uint32_t rs0 = 0, rph0 = 0, rs1 = 0, rph1 = 0;  // sub-ring positions (scalars: no local memory)
-      uint32_t xt = 0, tc = 0;
+      uint32_t xt = 0, xphase = 0, tc = 0;
       int j = 0;
       for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++j) {
         const int chunk = u / p.num_m;
@@ -328,13 +328,16 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
                           kb * BK, m * BM, pol_a);
         }
         for (int t = t0; t < t1; ++t, ++tc) {
-          const uint32_t ring = tc % nis;
+          const uint32_t ring = (nis == 2) ? (tc & 1) : 0;
           if (!IS_IP) {  // base norms of this tile -> ring slot (consumed by the epilogue)
-            const uint32_t xs = xt % xn_slots, xph = (xt / xn_slots) & 1;
+            const uint32_t xs = xt, xph = xphase;
+            if (++xt == (uint32_t)xn_slots) {
+              xt = 0;
+              xphase ^= 1;
+            }
             mbar_wait(&xempty[xs], xph ^ 1);
             mbar_arrive_expect_tx(&xfull[xs], BN * sizeof(float));
             bulk_load(xn_s + xs * BN, p.xnorm + (size_t)t * BN, BN * sizeof(float), &xfull[xs]);
-            ++xt;
           }
           for (int kb = 0; kb < num_kb; ++kb) {
             uint32_t& rs = ring ? rs1 : rs0;
@@ -385,7 +388,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
           tc_fence_after();
         }
         for (int t = t0; t < t1; ++t, ++tcount) {
-          if (tcount % nis != mw) continue;
+          if (nis == 2 && (tcount & 1) != mw) continue;
           const uint32_t buf = tcount & 1, tph = (tcount >> 1) & 1;
           const bool tr = p.trace != nullptr && blockIdx.x == 0 && tcount < 256;
           if (tr) p.trace[tcount * 16 + 0] = clock64();
@@ -457,7 +460,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     const int k = p.k;
     const int dp = num_kb * BK;
     const int a_cols = (MODE == 0) ? 2 * dp : dp / 2;  // TMEM columns of the query operand
-    uint32_t tcount = 0;
+    uint32_t tcount = 0, x_slot = 0, x_phase = 0;
     for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
       const int chunk = u / p.num_m;
       const int m = u - chunk * p.num_m;
@@ -549,7 +552,11 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
 
       for (int t = t0; t < t1; ++t, ++tcount) {
         const uint32_t buf = tcount & 1, tph = (tcount >> 1) & 1;
-        const uint32_t xslot = tcount % xn_slots, xph = (tcount / xn_slots) & 1;
+        const uint32_t xslot = x_slot, xph = x_phase;
+        if (++x_slot == (uint32_t)xn_slots) {
+          x_slot = 0;
+          x_phase ^= 1;
+        }
         const bool tr = p.trace != nullptr && blockIdx.x == 0 && tcount < 256 && ew == 0 && lane == 0;
         if (tr) p.trace[tcount * 16 + 4] = clock64();
         mbar_wait(&tfull[buf], tph);
@@ -562,46 +569,47 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         const float* xs = xn_s + xslot * BN + h * COLS;
         // Filter on f = xn - 2 ip (L2; one FMA) or -ip (IP) against T; the
         // exact reference value (qn + xn) - 2 ip is computed for survivors only.
-        auto process = [&](const uint32_t (&r)[32], int c0) {
-          float f[32];
-          float m;
-          if (IS_IP) {
+        auto chunk_f = [&](const uint32_t (&r)[32], int c0, float (&f)[32]) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(r[j]);
-            m = -reduce32<true>(f);  // min(-ip) = -max(ip)
-          } else {
-#pragma unroll
-            for (int j4 = 0; j4 < 8; ++j4) {
+          for (int j4 = 0; j4 < 8; ++j4) {
+            if (IS_IP) {
+              f[4 * j4 + 0] = __uint_as_float(r[4 * j4 + 0]);
+              f[4 * j4 + 1] = __uint_as_float(r[4 * j4 + 1]);
+              f[4 * j4 + 2] = __uint_as_float(r[4 * j4 + 2]);
+              f[4 * j4 + 3] = __uint_as_float(r[4 * j4 + 3]);
+            } else {
               const float4 x = lds_f4(xs + c0 + 4 * j4);
               f[4 * j4 + 0] = fmaf(-2.f, __uint_as_float(r[4 * j4 + 0]), x.x);
               f[4 * j4 + 1] = fmaf(-2.f, __uint_as_float(r[4 * j4 + 1]), x.y);
               f[4 * j4 + 2] = fmaf(-2.f, __uint_as_float(r[4 * j4 + 2]), x.z);
               f[4 * j4 + 3] = fmaf(-2.f, __uint_as_float(r[4 * j4 + 3]), x.w);
             }
-            m = reduce32<false>(f);
           }
-          if (!(m > T) && row_ok) {
-            const int lim = nvalid - c0;
-            const uint32_t valid = lim >= 32 ? 0xFFFFFFFFu : (lim <= 0 ? 0u : ((1u << lim) - 1u));
-            uint32_t cand = 0;
+        };
+        // rare path for one 32-column chunk: exact value + insertion per survivor
+        auto slow_chunk = [&](const uint32_t (&r)[32], int c0) {
+          float f[32];
+          chunk_f(r, c0, f);
+          const int lim = nvalid - c0;
+          const uint32_t valid = lim >= 32 ? 0xFFFFFFFFu : (lim <= 0 ? 0u : ((1u << lim) - 1u));
+          uint32_t cand = 0;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) cand |= ((IS_IP ? !(-f[j] > T) : !(f[j] > T)) ? 1u : 0u) << j;
-            cand &= valid;
-            while (cand) {
-              const int j = __ffs(cand) - 1;
-              cand &= cand - 1;
-              const float ip = select32(reinterpret_cast<const float(&)[32]>(r), j);
-              // flat.py:111: dmat = (qn + norms) - 2.0*ip  (2*ip exact -> one FMA)
-              float v = IS_IP ? -ip : fmaf(-2.f, ip, qn + lds_f32(xs + c0 + j));
-              if (!(v > thr)) {
-                if (!IS_IP) v = (v <= 0.f) ? 0.f : v;  // np.maximum(dmat, 0) (flat.py:112)
-                if constexpr (KQ > 0) {
-                  queue_insert<KQS>(keys, pos, monotone(v), static_cast<uint32_t>(n0 + c0 + j));
-                  thr = unmonotone(min(keys[KQS - 1], gkey));
-                  T = filter_bound(thr);
-                } else {
-                  mybuf[cnt++] = (static_cast<uint64_t>(monotone(v)) << 32) | static_cast<uint32_t>(n0 + c0 + j);
-                }
+          for (int j = 0; j < 32; ++j) cand |= ((IS_IP ? !(-f[j] > T) : !(f[j] > T)) ? 1u : 0u) << j;
+          cand &= valid;
+          while (cand) {
+            const int j = __ffs(cand) - 1;
+            cand &= cand - 1;
+            const float ip = select32(reinterpret_cast<const float(&)[32]>(r), j);
+            // flat.py:111: dmat = (qn + norms) - 2.0*ip  (2*ip exact -> one FMA)
+            float v = IS_IP ? -ip : fmaf(-2.f, ip, qn + lds_f32(xs + c0 + j));
+            if (!(v > thr)) {
+              if (!IS_IP) v = (v <= 0.f) ? 0.f : v;  // np.maximum(dmat, 0) (flat.py:112)
+              if constexpr (KQ > 0) {
+                queue_insert<KQS>(keys, pos, monotone(v), static_cast<uint32_t>(n0 + c0 + j));
+                thr = unmonotone(min(keys[KQS - 1], gkey));
+                T = filter_bound(thr);
+              } else {
+                mybuf[cnt++] = (static_cast<uint64_t>(monotone(v)) << 32) | static_cast<uint32_t>(n0 + c0 + j);
               }
             }
           }
@@ -626,13 +634,23 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             for (int j = 0; j < COLS; ++j)
               if (j < nvalid) p.dbg_ip[(size_t)row * p.nb + n0 + j] = __uint_as_float(racc[j]);
           }
+          // fast path: one straight-line block, a single branch per tile
+          float m = 0.f;
 #pragma unroll
           for (int c = 0; c < COLS / 32; ++c) {
-            process(*reinterpret_cast<const uint32_t(*)[32]>(&racc[32 * c]), c * 32);
-            if constexpr (KQ == 0) {
-              if (c & 1) compact_lanes(p.cap - 64);  // room for the next 64 columns
-            }
+            float f[32];
+            chunk_f(*reinterpret_cast<const uint32_t(*)[32]>(&racc[32 * c]), c * 32, f);
+            const float mc = IS_IP ? -reduce32<true>(f) : reduce32<false>(f);
+            m = (c == 0) ? mc : fmin_nan(m, mc);
           }
+          if (!(m > T) && row_ok) {  // divergent, rare
+#pragma unroll
+            for (int c = 0; c < COLS / 32; ++c)
+              slow_chunk(*reinterpret_cast<const uint32_t(*)[32]>(&racc[32 * c]), c * 32);
+          }
+          __syncwarp();
+          // warp-uniform: make room for the next tile's COLS candidates per row
+          if constexpr (KQ == 0) compact_lanes(p.cap - COLS);
         }
         __syncwarp();
         if (tr) p.trace[tcount * 16 + 7] = clock64();

@@ -14,11 +14,13 @@ ap.add_argument("--iters", type=int, default=2)
 ap.add_argument("--nq", type=int, default=0)
 ap.add_argument("--nb", type=int, default=0)
 ap.add_argument("--k", type=int, default=0)
+ap.add_argument("--storage", default="")
 a = ap.parse_args()
 cfg = dict(CONFIGS[a.config])
 if a.nq: cfg["nq"] = a.nq
 if a.nb: cfg["nb"] = a.nb
 if a.k: cfg["k"] = a.k
+if a.storage: cfg["storage"] = a.storage
 idx = FlatIndex(cfg["d"], METRIC_L2 if cfg["metric"] == "l2" else METRIC_IP, storage=cfg["storage"])
 step = 2_000_000
 for lo in range(0, cfg["nb"], step):
