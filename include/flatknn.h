@@ -113,9 +113,12 @@ const char* fk_last_error(void);
 int fk_set_profiling(fk_index* h, int on);
 int fk_kernel_times(fk_index* h, float* ms3, int* nlaunch);
 
-/* Tuning / introspection of the last search plan: grid size, number of
- * N-chunks (split-N), tile sizes, pipeline stages. */
-int fk_last_plan(fk_index* h, int* out8);
+/* Tuning / introspection of the last search plan, FK_PLAN_INTS ints: grid,
+ * N-chunks (split-N), tiles per chunk, work units, smem pipeline stages,
+ * query-operand mode, dynamic smem bytes, 100*queue+epilogue warps, TMEM
+ * accumulator buffers, epilogue warps, (reserved). */
+#define FK_PLAN_INTS 12
+int fk_last_plan(fk_index* h, int* out);
 
 #ifdef __cplusplus
 }

@@ -10,7 +10,7 @@ from __future__ import annotations
 import ctypes
 import os
 
-from .build import LIB_PATH
+from .build import DEV_LIB_PATH, LIB_PATH
 
 FK_METRIC_IP = 0
 FK_METRIC_L2 = 1
@@ -65,11 +65,12 @@ def lib() -> ctypes.CDLL:
     """Load (once) and return the CUDA library; raises if it was not built."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
+        path = DEV_LIB_PATH if os.environ.get("FK_DEV_LIB") == "1" else LIB_PATH
+        if not os.path.exists(path):
             raise ImportError(
-                f"{LIB_PATH} is missing: the CUDA extension is not built "
+                f"{path} is missing: the CUDA extension is not built "
                 "(run `python -m paper_2401_08281_b200.build`). There is no CPU fallback.")
-        L = ctypes.CDLL(LIB_PATH)
+        L = ctypes.CDLL(path)
         for name, (res, args) in _SIGS.items():
             fn = getattr(L, name)
             fn.restype = res

@@ -19,6 +19,9 @@ REPO = os.path.dirname(PKG_DIR)
 CSRC = os.path.join(PKG_DIR, "csrc")
 LIB_NAME = "libflatknn.so"
 LIB_PATH = os.path.join(PKG_DIR, LIB_NAME)
+# development variant (clock64 timeline trace + bottleneck flags, -DFK_DEV=1):
+# loaded instead of the product library only when FK_DEV_LIB=1 (scripts/)
+DEV_LIB_PATH = os.path.join(PKG_DIR, "libflatknn_dev.so")
 
 SOURCES = ["flatknn.cu"]
 DEPS = SOURCES + ["flatknn_kernels.cuh", "sm100.cuh"]
@@ -31,17 +34,18 @@ def nvcc_path() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def needs_build() -> bool:
-    if not os.path.exists(LIB_PATH):
+def needs_build(path: str = LIB_PATH) -> bool:
+    if not os.path.exists(path):
         return True
-    t = os.path.getmtime(LIB_PATH)
+    t = os.path.getmtime(path)
     deps = [os.path.join(CSRC, f) for f in DEPS] + [os.path.join(REPO, "include", "flatknn.h")]
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 
 
-def build(force: bool = False, verbose: bool = True) -> str:
-    if not force and not needs_build():
-        return LIB_PATH
+def build(force: bool = False, verbose: bool = True, dev: bool = False) -> str:
+    out = DEV_LIB_PATH if dev else LIB_PATH
+    if not force and not needs_build(out):
+        return out
     cmd = [
         nvcc_path(),
         "-gencode", "arch=compute_100a,code=sm_100a",
@@ -49,19 +53,19 @@ def build(force: bool = False, verbose: bool = True) -> str:
         "-Xcompiler", "-fPIC,-O3", "-shared", "-cudart", "static",
         "-Xptxas", "-v",
         "-I", os.path.join(REPO, "include"),
-        "-o", LIB_PATH + ".tmp",
-    ] + [os.path.join(CSRC, s) for s in SOURCES]
+        "-o", out + ".tmp",
+    ] + (["-DFK_DEV=1"] if dev else []) + [os.path.join(CSRC, s) for s in SOURCES]
     if verbose:
         print("[build]", " ".join(cmd), file=sys.stderr)
     res = subprocess.run(cmd, capture_output=True, text=True)
-    log_path = os.path.join(PKG_DIR, "build.log")
+    log_path = os.path.join(PKG_DIR, "build_dev.log" if dev else "build.log")
     with open(log_path, "w") as f:
         f.write(res.stdout + res.stderr)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed (see {log_path}):\n{res.stderr[-4000:]}")
-    os.replace(LIB_PATH + ".tmp", LIB_PATH)
-    return LIB_PATH
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv))
+    print(build(force="--force" in sys.argv, dev="--dev" in sys.argv))

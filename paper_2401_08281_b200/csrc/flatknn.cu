@@ -90,7 +90,7 @@ int make_map(CUtensorMap* m, const void* base, int elem_bytes, uint64_t cols, ui
 
 constexpr int FK_MAX_K = 2048;
 constexpr int MERGE_SMC = 16384;    // large-k merge: survivors gathered in smem (128 KB) + 2048 winners
-constexpr int SMEM_LIMIT = 232448;  // sm_100 max dynamic smem per block (227 KB)
+constexpr int SMEM_LIMIT = 232448 - 1024;  // sm_100 227 KB per block, minus the static barrier block
 constexpr int SMEM_RESERVE = 1024 /*align*/ + 512 /*barriers + tmem slot*/;
 
 int elem_bytes_of(int storage) { return storage == FK_F32 ? 4 : 2; }
@@ -123,6 +123,7 @@ struct DevBuf {
 
 struct fk_index {
   int device = 0, d = 0, dp = 0, metric = FK_METRIC_L2, storage = FK_F32;
+  int fold = 0;  // bf16 L2 with d+3 <= dp: norms folded into the GEMM operands (MODE 3 kernels)
   int64_t ntotal = 0, cap = 0;
   void* s0 = nullptr;        // stored operand (hi / f16 / bf16) [cap][dp]
   void* s1 = nullptr;        // lo part (fp32 mode) [cap][dp]
@@ -140,7 +141,7 @@ struct fk_index {
   size_t ev_used = 0;
   int nlaunch = 0;        // launches of the last search
   long long nlaunch_acc = 0;  // launches since the last fk_kernel_times
-  int plan[8] = {0};
+  int plan[FK_PLAN_INTS] = {0};
   float* dbg_ip = nullptr;  // test hook (FK_DEBUG_IP)
   unsigned long long* trace = nullptr;  // debug timeline hook
 };
@@ -200,16 +201,16 @@ int grow(fk_index* h, int64_t need, cudaStream_t st) {
 }
 
 int launch_prep(int storage, const void* x, int dtype, int64_t n, int d, int dp, void* o0, void* o1, float* norms,
-                int64_t row0, cudaStream_t st) {
+                int64_t row0, cudaStream_t st, int fold = 0) {
   if (n <= 0) return FK_OK;
   const int wpb = 8;
   const unsigned grid = (unsigned)((n + wpb - 1) / wpb);
   if (storage == FK_F32)
-    prep_rows_kernel<0><<<grid, wpb * 32, 0, st>>>(x, dtype, n, d, dp, o0, o1, norms, row0);
+    prep_rows_kernel<0><<<grid, wpb * 32, 0, st>>>(x, dtype, n, d, dp, o0, o1, norms, row0, 0);
   else if (storage == FK_F16)
-    prep_rows_kernel<1><<<grid, wpb * 32, 0, st>>>(x, dtype, n, d, dp, o0, o1, norms, row0);
+    prep_rows_kernel<1><<<grid, wpb * 32, 0, st>>>(x, dtype, n, d, dp, o0, o1, norms, row0, 0);
   else
-    prep_rows_kernel<2><<<grid, wpb * 32, 0, st>>>(x, dtype, n, d, dp, o0, o1, norms, row0);
+    prep_rows_kernel<2><<<grid, wpb * 32, 0, st>>>(x, dtype, n, d, dp, o0, o1, norms, row0, fold);
   CKL();
   return FK_OK;
 }
@@ -243,7 +244,7 @@ int launch_fused_k(int kq, const CUtensorMap& a0, const CUtensorMap& a1, const C
 }
 
 template <int EPI>
-int launch_fused_e(int storage, bool ip, int kq, const CUtensorMap& a0, const CUtensorMap& a1,
+int launch_fused_e(int storage, bool fold, bool ip, int kq, const CUtensorMap& a0, const CUtensorMap& a1,
                    const CUtensorMap& b0, const CUtensorMap& b1, const SearchParams& sp, int grid, int smem,
                    cudaStream_t st) {
   if (storage == FK_F32)
@@ -252,15 +253,16 @@ int launch_fused_e(int storage, bool ip, int kq, const CUtensorMap& a0, const CU
   if (storage == FK_F16)
     return ip ? launch_fused_k<1, true, EPI>(kq, a0, a1, b0, b1, sp, grid, smem, st)
               : launch_fused_k<1, false, EPI>(kq, a0, a1, b0, b1, sp, grid, smem, st);
+  if (fold && !ip) return launch_fused_k<3, false, EPI>(kq, a0, a1, b0, b1, sp, grid, smem, st);
   return ip ? launch_fused_k<2, true, EPI>(kq, a0, a1, b0, b1, sp, grid, smem, st)
             : launch_fused_k<2, false, EPI>(kq, a0, a1, b0, b1, sp, grid, smem, st);
 }
 
-int launch_fused(int epi, int storage, bool ip, int kq, const CUtensorMap& a0, const CUtensorMap& a1,
+int launch_fused(int epi, int storage, bool fold, bool ip, int kq, const CUtensorMap& a0, const CUtensorMap& a1,
                  const CUtensorMap& b0, const CUtensorMap& b1, const SearchParams& sp, int grid, int smem,
                  cudaStream_t st) {
-  if (epi == 8) return launch_fused_e<8>(storage, ip, kq, a0, a1, b0, b1, sp, grid, smem, st);
-  return launch_fused_e<4>(storage, ip, kq, a0, a1, b0, b1, sp, grid, smem, st);
+  if (epi == 8) return launch_fused_e<8>(storage, fold, ip, kq, a0, a1, b0, b1, sp, grid, smem, st);
+  return launch_fused_e<4>(storage, fold, ip, kq, a0, a1, b0, b1, sp, grid, smem, st);
 }
 
 // Split-N plan: choose the number of N-chunks S so that num_m*S work units
@@ -322,6 +324,10 @@ int fk_create(int device, int d, int metric, int storage, fk_index** out) {
   h->dp = (d + ce - 1) / ce * ce;
   h->metric = metric;
   h->storage = storage;
+  // bf16 L2 with >= 3 free padding columns: fold the norms into the operands
+  // (FK_NO_FOLD=1 keeps the separate norm tile; tests compare both layouts)
+  h->fold = storage == FK_BF16 && metric == FK_METRIC_L2 && d + 3 <= h->dp;
+  if (const char* e = getenv("FK_NO_FOLD"); e && atoi(e)) h->fold = 0;
   h->num_sms = prop.multiProcessorCount;
   if (cudaMalloc((void**)&h->xn_max, sizeof(float)) != cudaSuccess || cudaMemset(h->xn_max, 0, sizeof(float)) != cudaSuccess) {
     delete h;
@@ -386,7 +392,8 @@ int fk_add(fk_index* h, const void* x, int64_t n, int dtype, const int64_t* ids,
       CK(cudaMemcpyAsync(h->stage_in.p, src, m * in_row, cudaMemcpyHostToDevice, st));
       src = h->stage_in.p;
     }
-    if ((rc = launch_prep(h->storage, src, dtype, m, h->d, h->dp, h->s0, h->s1, h->norms, h->ntotal + r0, st)))
+    if ((rc = launch_prep(h->storage, src, dtype, m, h->d, h->dp, h->s0, h->s1, h->norms, h->ntotal + r0, st,
+                          h->fold ? 1 : 0)))
       return rc;
     if (!on_device) CK(cudaStreamSynchronize(st));  // stage buffer reused by the next slice
   }
@@ -410,7 +417,8 @@ int fk_add(fk_index* h, const void* x, int64_t n, int dtype, const int64_t* ids,
 namespace {
 
 struct Plan {
-  int kq, epi, nh, num_m, n_tiles, S, chunk_tiles, num_units, grid, a_mode, stages, smem, S_tot, cap, xn_slots;
+  int kq, epi, nh, num_m, n_tiles, S, chunk_tiles, num_units, grid, a_mode, stages, smem, S_tot, cap, xn_slots,
+      acc_stages;
 };
 
 // Tile / split-N / pipeline plan for one fused pass over base rows [0, nb_pass).
@@ -441,7 +449,7 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   if (P.a_mode == 0 && a_tmem_cols > 256) P.a_mode = 1;
   const int hist_bytes = kq == 0 ? P.epi * 1024 : 0;
   // norm-tile ring: 3 slots when smem is tight (fp32), 8 otherwise
-  P.xn_slots = (h->storage == FK_F32 && P.a_mode != 2) ? 3 : 8;
+  P.xn_slots = (h->metric == FK_METRIC_IP || h->fold) ? 0 : (h->storage == FK_F32 && P.a_mode != 2) ? 3 : 8;
   const int xn_bytes = P.xn_slots * BN * 4;
   auto stages_for = [&](int mode) {
     const int avail = SMEM_LIMIT - SMEM_RESERVE - hist_bytes - xn_bytes - (mode == 1 ? a_bytes : 0);
@@ -452,9 +460,12 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
     P.a_mode = 2;
     P.stages = stages_for(2);
   }
-  P.stages = std::min(P.stages, 8);
+  P.stages = std::min(P.stages, MAX_STAGES);
   if (const char* e = getenv("FK_STAGES")) P.stages = std::max(2, std::min(P.stages, atoi(e)));
   if (P.stages < 2) return set_err(FK_E_UNSUPPORTED, "pipeline does not fit in shared memory");
+  // TMEM: 512 columns = acc_stages x 128-column accumulators (+ the query operand in a_mode 0)
+  P.acc_stages = std::min(4, (512 - (P.a_mode == 0 ? a_tmem_cols : 0)) / BN);
+  if (const char* e = getenv("FK_ACC")) P.acc_stages = std::max(2, std::min(P.acc_stages, atoi(e)));
   P.smem = SMEM_RESERVE + hist_bytes + xn_bytes + (P.a_mode == 1 ? a_bytes : 0) +
            P.stages * (P.a_mode == 2 ? 2 : 1) * split * (int)CHUNK_BYTES;
   P.S_tot = P.S * P.nh;
@@ -511,10 +522,16 @@ int run_fused(fk_index* h, const Plan& P, int64_t nq, int64_t nb_pass, int k, bo
   sp.a_mode = P.a_mode;
   sp.stages = P.stages;
   sp.xn_slots = P.xn_slots;
+  sp.acc_stages = P.acc_stages;
+  {
+    const int bk = chunk_elems_of(h->storage), kstep = h->storage == FK_F32 ? 8 : 16;
+    const int last = h->d + (h->fold ? 3 : 0) - (sp.num_kb - 1) * bk;  // K elements in the last chunk (1..bk)
+    sp.kk_last = (last + kstep - 1) / kstep;
+  }
   sp.n_issuers = P.stages >= 4 ? 2 : 1;  // each issuer needs a sub-ring of >= 2 slots
   if (const char* e = getenv("FK_ISSUERS")) sp.n_issuers = (atoi(e) == 1 || P.stages < 4) ? 1 : 2;
   if (const char* e = getenv("FK_DEBUG_FLAGS")) sp.dbg_flags = atoi(e);
-  rc = launch_fused(P.epi, h->storage, ip, P.kq, ta0, ta1, tb0, tb1, sp, P.grid, P.smem, st);
+  rc = launch_fused(P.epi, h->storage, h->fold != 0, ip, P.kq, ta0, ta1, tb0, tb1, sp, P.grid, P.smem, st);
   if (rc == FK_OK) h->nlaunch++;
   return rc;
 }
@@ -615,7 +632,7 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
     if ((rc = h->qn.ensure(nq * sizeof(float)))) return rc;
     if (ev) CK(cudaEventRecord(ev[0], st));
     if ((rc = launch_prep(h->storage, qsrc, dtype, nq, h->d, h->dp, h->q0.p, h->q1.p, static_cast<float*>(h->qn.p),
-                          0, st)))
+                          0, st, h->fold ? 2 : 0)))
       return rc;
     h->nlaunch++;
 
@@ -663,6 +680,8 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
     h->plan[5] = pl.a_mode;
     h->plan[6] = pl.smem;
     h->plan[7] = kq * 100 + pl.epi;
+    h->plan[8] = pl.acc_stages;
+    h->plan[9] = pl.epi;
   }
 
   if (!on_device) {
@@ -711,9 +730,12 @@ int fk_reconstruct(fk_index* h, const int64_t* positions, int64_t n, float* out,
     dout = static_cast<float*>(h->stage_in.p);
   }
   const unsigned grid = (unsigned)((n + 7) / 8);
-  if (h->storage == FK_F32) reconstruct_kernel<0><<<grid, 256, 0, st>>>(h->s0, h->s1, h->dp, h->d, dpos, n, dout);
-  else if (h->storage == FK_F16) reconstruct_kernel<1><<<grid, 256, 0, st>>>(h->s0, h->s1, h->dp, h->d, dpos, n, dout);
-  else reconstruct_kernel<2><<<grid, 256, 0, st>>>(h->s0, h->s1, h->dp, h->d, dpos, n, dout);
+  if (h->storage == FK_F32)
+    reconstruct_kernel<0><<<grid, 256, 0, st>>>(h->s0, h->s1, h->dp, h->d, dpos, n, dout, 1.f);
+  else if (h->storage == FK_F16)
+    reconstruct_kernel<1><<<grid, 256, 0, st>>>(h->s0, h->s1, h->dp, h->d, dpos, n, dout, 1.f);
+  else
+    reconstruct_kernel<2><<<grid, 256, 0, st>>>(h->s0, h->s1, h->dp, h->d, dpos, n, dout, h->fold ? -0.5f : 1.f);
   CKL();
   if (!on_device) {
     CK(cudaMemcpyAsync(out, dout, n * (size_t)h->d * sizeof(float), cudaMemcpyDeviceToHost, st));
@@ -804,9 +826,9 @@ int fk_kernel_times(fk_index* h, float* ms3, int* nlaunch) {
   return FK_OK;
 }
 
-int fk_last_plan(fk_index* h, int* out8) {
-  if (!h || !out8) return set_err(FK_E_INVALID, "NULL argument");
-  std::memcpy(out8, h->plan, sizeof(h->plan));
+int fk_last_plan(fk_index* h, int* out) {
+  if (!h || !out) return set_err(FK_E_INVALID, "NULL argument");
+  std::memcpy(out, h->plan, sizeof(h->plan));
   return FK_OK;
 }
 

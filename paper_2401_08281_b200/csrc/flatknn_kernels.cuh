@@ -19,6 +19,12 @@
 
 #include "sm100.cuh"
 
+// FK_DEV=1 (libflatknn_dev.so, scripts only) compiles in the clock64 timeline
+// trace and the bottleneck-experiment flags; the product build has neither.
+#ifndef FK_DEV
+#define FK_DEV 0
+#endif
+
 namespace fk {
 
 constexpr int BM = 128;                        // queries per tile (TMEM lanes)
@@ -60,6 +66,8 @@ struct SearchParams {
   int xn_slots;    // base-norm tile ring depth (prefetched by the producer)
   unsigned long long* trace;  // debug timeline (CTA 0): [tile][16] clock64 stamps
   int n_issuers;   // MMA-issuing threads (warps 1 and 3)
+  int acc_stages;  // TMEM accumulator buffers (2..4); the query operand (a_mode 0) follows them
+  int kk_last;     // MMA K-steps in the last 128-byte K-chunk (trims the zero padding of d)
   int dbg_flags;   // bottleneck experiments: 1 = epilogue skips compute, 2 = producer skips TMA
 };
 
@@ -201,7 +209,8 @@ __device__ __forceinline__ int warp_compact_le(uint64_t* buf, int cnt, uint64_t 
 // a_mode 0: queries in TMEM (TS MMA; frees smem, halves smem operand reads)
 // a_mode 1: queries resident in smem for the unit
 // a_mode 2: queries streamed with every B stage (large d)
-constexpr int TMEM_A_COL = 2 * BN;  // A operand columns start after the accumulators
+constexpr int MAX_ACC = 4;      // TMEM accumulator buffers
+constexpr int MAX_STAGES = 16;  // smem operand ring  // TMEM accumulator buffers (runtime p.acc_stages); A operand columns follow them
 
 // NaN-propagating min / max over 32 values with 3-input FMNMX (16 instructions).
 template <bool MAX>
@@ -240,6 +249,11 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
   constexpr int SPLIT = (MODE == 0) ? 2 : 1;
   constexpr int BK = (MODE == 0) ? 32 : 64;  // elements per 128-byte K-chunk
   constexpr uint32_t AB_FMT = (MODE == 0) ? 2u : (MODE == 1 ? 0u : 1u);
+  // MODE 3 (bf16, L2): base rows are stored as [-2x | xn split in 3 bf16] and
+  // query rows as [q | 1 1 1], so the accumulator already holds xn - 2 q.x and
+  // the epilogue needs no base-norm tile (FOLD).
+  constexpr bool FOLD = (MODE == 3);
+  constexpr bool XN_TILE = !IS_IP && !FOLD;
   constexpr uint32_t IDESC = make_idesc(AB_FMT, BM, BN);
   constexpr int NH = EPI / 4;       // epilogue warps per TMEM lane quarter
   constexpr int COLS = BN / NH;     // accumulator columns per epilogue warp
@@ -254,23 +268,27 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
   const int a_mode = p.a_mode;
   const uint32_t a_bytes = (a_mode == 1) ? SPLIT * num_kb * CHUNK_BYTES : 0u;
   const uint32_t stage_bytes = (a_mode == 2 ? 2 * SPLIT : SPLIT) * CHUNK_BYTES;
-  const uint32_t tmem_cols = (a_mode == 0) ? 512u : 256u;
+  constexpr uint32_t tmem_cols = 512u;  // 1 CTA per SM: take the whole TMEM
 
   uint8_t* a_region = smem;
   uint8_t* st_region = smem + a_bytes;
   const int xn_slots = p.xn_slots;
   float* xn_s = reinterpret_cast<float*>(st_region + stages * stage_bytes);  // [xn_slots][BN]
   uint32_t* hist_base = reinterpret_cast<uint32_t*>(xn_s + xn_slots * BN);  // large-k: [EPI][256]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(hist_base + (KQ == 0 ? EPI * 256 : 0));
-  uint64_t* full = bars;         // [8]
-  uint64_t* empty = bars + 8;    // [8]
-  uint64_t* tfull = bars + 16;   // [2]
-  uint64_t* tempty = bars + 18;  // [2]
-  uint64_t* xfull = bars + 20;   // [8]
-  uint64_t* xempty = bars + 28;  // [8]
-  uint64_t* afull = bars + 36;
-  uint64_t* aempty = bars + 37;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 38);
+  // barriers live in static shared memory: constant addresses, nothing to
+  // rematerialise inside the hot loops
+  __shared__ __align__(8) uint64_t bars[60];
+  uint64_t* full = bars;         // [MAX_STAGES]
+  uint64_t* empty = bars + 16;   // [MAX_STAGES]
+  uint64_t* tfull = bars + 32;   // [MAX_ACC]
+  uint64_t* tempty = bars + 36;  // [MAX_ACC]
+  uint64_t* xfull = bars + 40;   // [8]
+  uint64_t* xempty = bars + 48;  // [8]
+  uint64_t* afull = bars + 56;
+  uint64_t* aempty = bars + 57;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 58);
+  const uint32_t acc_stages = p.acc_stages;
+  const uint32_t tmem_a_col = acc_stages * BN;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_b0);
@@ -285,7 +303,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < (int)acc_stages; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], EPI);
     }
@@ -329,7 +347,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         }
         for (int t = t0; t < t1; ++t, ++tc) {
           const uint32_t ring = (nis == 2) ? (tc & 1) : 0;
-          if (!IS_IP) {  // base norms of this tile -> ring slot (consumed by the epilogue)
+          if (XN_TILE) {  // base norms of this tile -> ring slot (consumed by the epilogue)
             const uint32_t xs = xt, xph = xphase;
             if (++xt == (uint32_t)xn_slots) {
               xt = 0;
@@ -348,7 +366,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
               rph ^= 1;
             }
             mbar_wait(&empty[stage], phase ^ 1);
-            if (p.dbg_flags & 2) {  // experiment: no data movement
+            if (FK_DEV && (p.dbg_flags & 2)) {  // experiment: no data movement
               mbar_arrive(&full[stage]);
               continue;
             }
@@ -366,19 +384,23 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       }
     }
   } else if (warp == 1 || (warp == 3 && p.n_issuers == 2)) {
-    // ===================== MMA issuers (one thread each) =====================
+    // ===================== MMA issuers (whole warp, one elected lane issues) =====================
     // With two issuers (warps 1 and 3), issuer w owns the tiles with
-    // tcount % 2 == w and hence accumulator buffer w: while one waits on its
-    // barriers the other keeps the tensor pipe fed.
-    if (lane == 0) {
+    // tcount % 2 == w: while one waits on its barriers the other keeps the
+    // tensor pipe fed.  The loop runs on all 32 lanes so every descriptor is
+    // warp-uniform; elect_one() picks the lane that issues.
+    {
       const uint32_t nis = p.n_issuers;
       const uint32_t mw = (warp == 1) ? 0u : 1u;
       const uint32_t sh = (uint32_t)stages / nis;
       uint32_t rslot = 0, rphase = 0;  // position in this issuer's sub-ring
-      uint32_t tcount = 0;
+      uint32_t tcount = 0, buf = 0, tph = 0;  // accumulator ring position of tile tcount
       int j = 0;
-      const uint32_t a_tm = tmem_base + TMEM_A_COL;
+      const uint32_t a_tm = tmem_base + tmem_a_col;
       const uint32_t a_lo_off = (MODE == 0) ? (uint32_t)(num_kb * 32) : 0u;  // lo half after hi (columns)
+      const uint64_t st_desc0 = smem_desc_sw128(smem_u32(st_region));
+      const uint64_t a_desc0 = smem_desc_sw128(smem_u32(a_region));
+      const int kk_last = p.kk_last;
       for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++j) {
         const int chunk = u / p.num_m;
         const int t0 = chunk * p.chunk_tiles;
@@ -388,15 +410,20 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
           tc_fence_after();
         }
         for (int t = t0; t < t1; ++t, ++tcount) {
+          const uint32_t cbuf = buf, cph = tph;
+          if (++buf == acc_stages) {
+            buf = 0;
+            tph ^= 1;
+          }
           if (nis == 2 && (tcount & 1) != mw) continue;
-          const uint32_t buf = tcount & 1, tph = (tcount >> 1) & 1;
-          const bool tr = p.trace != nullptr && blockIdx.x == 0 && tcount < 256;
+          const bool tr = FK_DEV && p.trace != nullptr && blockIdx.x == 0 && tcount < 256 && lane == 0;
           if (tr) p.trace[tcount * 16 + 0] = clock64();
-          mbar_wait(&tempty[buf], tph ^ 1);
+          mbar_wait(&tempty[cbuf], cph ^ 1);
           tc_fence_after();
           if (tr) p.trace[tcount * 16 + 1] = clock64();
-          const uint32_t d_tmem = tmem_base + buf * BN;
+          const uint32_t d_tmem = tmem_base + cbuf * BN;
           for (int kb = 0; kb < num_kb; ++kb) {
+            const int nkk = (kb == num_kb - 1) ? kk_last : 4;  // skip all-zero K padding steps
             const uint32_t stage = mw * sh + rslot, phase = rphase;
             if (++rslot == sh) {
               rslot = 0;
@@ -405,50 +432,62 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             mbar_wait(&full[stage], phase);
             tc_fence_after();
             if (tr && kb < 4) p.trace[tcount * 16 + 13 + (kb < 3 ? kb : 2)] = clock64();
-            uint8_t* sb = st_region + stage * stage_bytes;
-            const uint64_t bd0 = smem_desc_sw128(smem_u32(sb));
-            if (a_mode == 0) {
-              const uint32_t ah = a_tm + kb * 32;
-              if (MODE == 0) {
-                const uint64_t bd1 = smem_desc_sw128(smem_u32(sb + CHUNK_BYTES));
+            // descriptor start address is in 16-byte units (bits 0-13)
+            const uint64_t bd0 = st_desc0 + ((stage * stage_bytes) >> 4);
+            const uint64_t bd1 = bd0 + (CHUNK_BYTES >> 4);
+            if (elect_one()) {
+              if (a_mode == 0) {
+                const uint32_t ah = a_tm + kb * 32;
+                if (MODE == 0) {
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
-                  const uint64_t off = 2 * kk;  // 32 B = K 8 (tf32) per step, 16-byte units
-                  mma_tf32_ts(d_tmem, ah + a_lo_off + 8 * kk, bd0 + off, IDESC, (kb | kk) != 0);  // lo*hi
-                  mma_tf32_ts(d_tmem, ah + 8 * kk, bd1 + off, IDESC, 1u);                        // hi*lo
-                  mma_tf32_ts(d_tmem, ah + 8 * kk, bd0 + off, IDESC, 1u);                        // hi*hi
+                  for (int kk = 0; kk < 4; ++kk) {
+                    if (kk >= nkk) break;
+                    const uint64_t off = 2 * kk;  // 32 B = K 8 (tf32) per step, 16-byte units
+                    mma_tf32_ts(d_tmem, ah + a_lo_off + 8 * kk, bd0 + off, IDESC, (kb | kk) != 0);  // lo*hi
+                    mma_tf32_ts(d_tmem, ah + 8 * kk, bd1 + off, IDESC, 1u);                        // hi*lo
+                    mma_tf32_ts(d_tmem, ah + 8 * kk, bd0 + off, IDESC, 1u);                        // hi*hi
+                  }
+                } else {
+#pragma unroll
+                  for (int kk = 0; kk < 4; ++kk) {
+                    if (kk >= nkk) break;
+                    mma_f16_ts(d_tmem, ah + 8 * kk, bd0 + 2 * kk, IDESC, (kb | kk) != 0);
+                  }
                 }
               } else {
+                const uint64_t ad0 = (a_mode == 1) ? a_desc0 + ((kb * CHUNK_BYTES) >> 4) : bd0 + ((SPLIT * CHUNK_BYTES) >> 4);
+                if (MODE == 0) {
+                  const uint64_t ad1 = (a_mode == 1) ? a_desc0 + (((num_kb + kb) * CHUNK_BYTES) >> 4)
+                                                     : bd0 + ((3 * CHUNK_BYTES) >> 4);
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk)
-                  mma_f16_ts(d_tmem, ah + 8 * kk, bd0 + 2 * kk, IDESC, (kb | kk) != 0);
-              }
-            } else {
-              const uint8_t* a0 = (a_mode == 1) ? a_region + kb * CHUNK_BYTES : sb + SPLIT * CHUNK_BYTES;
-              const uint64_t ad0 = smem_desc_sw128(smem_u32(a0));
-              if (MODE == 0) {
-                const uint8_t* a1 = (a_mode == 1) ? a_region + (num_kb + kb) * CHUNK_BYTES : sb + 3 * CHUNK_BYTES;
-                const uint64_t ad1 = smem_desc_sw128(smem_u32(a1));
-                const uint64_t bd1 = smem_desc_sw128(smem_u32(sb + CHUNK_BYTES));
+                  for (int kk = 0; kk < 4; ++kk) {
+                    if (kk >= nkk) break;
+                    const uint64_t off = 2 * kk;
+                    mma_tf32(d_tmem, ad1 + off, bd0 + off, IDESC, (kb | kk) != 0);
+                    mma_tf32(d_tmem, ad0 + off, bd1 + off, IDESC, 1u);
+                    mma_tf32(d_tmem, ad0 + off, bd0 + off, IDESC, 1u);
+                  }
+                } else {
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
-                  const uint64_t off = 2 * kk;
-                  mma_tf32(d_tmem, ad1 + off, bd0 + off, IDESC, (kb | kk) != 0);
-                  mma_tf32(d_tmem, ad0 + off, bd1 + off, IDESC, 1u);
-                  mma_tf32(d_tmem, ad0 + off, bd0 + off, IDESC, 1u);
+                  for (int kk = 0; kk < 4; ++kk) {
+                    if (kk >= nkk) break;
+                    mma_f16(d_tmem, ad0 + 2 * kk, bd0 + 2 * kk, IDESC, (kb | kk) != 0);
+                  }
                 }
-              } else {
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk) mma_f16(d_tmem, ad0 + 2 * kk, bd0 + 2 * kk, IDESC, (kb | kk) != 0);
               }
+              mma_commit(&empty[stage]);
             }
-            mma_commit(&empty[stage]);
+            __syncwarp();
             if (tr && kb < 4) p.trace[tcount * 16 + 9 + kb] = clock64();
           }
-          mma_commit(&tfull[buf]);
+          if (elect_one()) mma_commit(&tfull[cbuf]);
+          __syncwarp();
           if (tr) p.trace[tcount * 16 + 3] = clock64();
         }
-        if (a_mode == 1) mma_commit(aempty);
+        if (a_mode == 1) {
+          if (elect_one()) mma_commit(aempty);
+          __syncwarp();
+        }
       }
     }
   } else if (warp >= EPI_WARP0) {
@@ -460,7 +499,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     const int k = p.k;
     const int dp = num_kb * BK;
     const int a_cols = (MODE == 0) ? 2 * dp : dp / 2;  // TMEM columns of the query operand
-    uint32_t tcount = 0, x_slot = 0, x_phase = 0;
+    uint32_t tcount = 0, x_slot = 0, x_phase = 0, a_buf = 0, a_ph = 0;
     for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
       const int chunk = u / p.num_m;
       const int m = u - chunk * p.num_m;
@@ -489,7 +528,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             v[4 * i + 2] = w.z;
             v[4 * i + 3] = w.w;
           }
-          tmem_st_32x32b_x32(tmem_base + lane_addr + TMEM_A_COL + cc * 32, v);
+          tmem_st_32x32b_x32(tmem_base + lane_addr + tmem_a_col + cc * 32, v);
         }
         tmem_st_wait();
         tc_fence_before();
@@ -551,17 +590,21 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       };
 
       for (int t = t0; t < t1; ++t, ++tcount) {
-        const uint32_t buf = tcount & 1, tph = (tcount >> 1) & 1;
+        const uint32_t buf = a_buf, tph = a_ph;
+        if (++a_buf == acc_stages) {
+          a_buf = 0;
+          a_ph ^= 1;
+        }
         const uint32_t xslot = x_slot, xph = x_phase;
         if (++x_slot == (uint32_t)xn_slots) {
           x_slot = 0;
           x_phase ^= 1;
         }
-        const bool tr = p.trace != nullptr && blockIdx.x == 0 && tcount < 256 && ew == 0 && lane == 0;
+        const bool tr = FK_DEV && p.trace != nullptr && blockIdx.x == 0 && tcount < 256 && ew == 0 && lane == 0;
         if (tr) p.trace[tcount * 16 + 4] = clock64();
         mbar_wait(&tfull[buf], tph);
         if (tr) p.trace[tcount * 16 + 5] = clock64();
-        if (!IS_IP) mbar_wait(&xfull[xslot], xph);
+        if (XN_TILE) mbar_wait(&xfull[xslot], xph);
         tc_fence_after();
         if (tr) p.trace[tcount * 16 + 6] = clock64();
         const int n0 = t * BN + h * COLS;
@@ -572,7 +615,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         auto chunk_f = [&](const uint32_t (&r)[32], int c0, float (&f)[32]) {
 #pragma unroll
           for (int j4 = 0; j4 < 8; ++j4) {
-            if (IS_IP) {
+            if (IS_IP || FOLD) {
               f[4 * j4 + 0] = __uint_as_float(r[4 * j4 + 0]);
               f[4 * j4 + 1] = __uint_as_float(r[4 * j4 + 1]);
               f[4 * j4 + 2] = __uint_as_float(r[4 * j4 + 2]);
@@ -600,8 +643,12 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             const int j = __ffs(cand) - 1;
             cand &= cand - 1;
             const float ip = select32(reinterpret_cast<const float(&)[32]>(r), j);
-            // flat.py:111: dmat = (qn + norms) - 2.0*ip  (2*ip exact -> one FMA)
-            float v = IS_IP ? -ip : fmaf(-2.f, ip, qn + lds_f32(xs + c0 + j));
+            // flat.py:111: dmat = (qn + norms) - 2.0*ip  (2*ip exact -> one FMA;
+            // FOLD: the accumulator already is xn - 2 ip)
+            float v;
+            if (IS_IP) v = -ip;
+            else if (FOLD) v = qn + ip;
+            else v = fmaf(-2.f, ip, qn + lds_f32(xs + c0 + j));
             if (!(v > thr)) {
               if (!IS_IP) v = (v <= 0.f) ? 0.f : v;  // np.maximum(dmat, 0) (flat.py:112)
               if constexpr (KQ > 0) {
@@ -617,7 +664,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         // (1) pull this warp's accumulator slice into registers, (2) hand the
         // TMEM buffer straight back to the MMA issuer, (3) filter + select from
         // registers while the tensor pipe already fills the buffer again.
-        const bool do_epi = !(p.dbg_flags & 1);
+        const bool do_epi = !(FK_DEV && (p.dbg_flags & 1));
         uint32_t racc[COLS];
         if (do_epi) {
 #pragma unroll
@@ -643,7 +690,12 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             const float mc = IS_IP ? -reduce32<true>(f) : reduce32<false>(f);
             m = (c == 0) ? mc : fmin_nan(m, mc);
           }
-          if (!(m > T) && row_ok) {  // divergent, rare
+          const bool slow = !(m > T) && row_ok && !(FK_DEV && (p.dbg_flags & 4));
+          if (FK_DEV && p.trace != nullptr) {
+            const unsigned sb = __ballot_sync(FULLMASK, slow);
+            if (tr) p.trace[tcount * 16 + 8] = __popc(sb);
+          }
+          if (slow) {  // divergent, rare
 #pragma unroll
             for (int c = 0; c < COLS / 32; ++c)
               slow_chunk(*reinterpret_cast<const uint32_t(*)[32]>(&racc[32 * c]), c * 32);
@@ -654,7 +706,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         }
         __syncwarp();
         if (tr) p.trace[tcount * 16 + 7] = clock64();
-        if (lane == 0 && !IS_IP) mbar_arrive(&xempty[xslot]);
+        if (lane == 0 && XN_TILE) mbar_arrive(&xempty[xslot]);
         if (((t - t0) & 15) == 15 && row_ok) {  // publish own k-th, fetch the shared bound
           const uint32_t mine = own_key();
           gkey = min(atomicMin(p.thr_key + row, mine), mine);
@@ -992,10 +1044,13 @@ __device__ __forceinline__ float tf32_rna(float v) {
 // One warp per row: convert n rows of `x` (row-major n x d, dtype in_dtype)
 // into the stored layout at rows [row0, row0+n) of out0/out1 (dp columns,
 // zero padded), and write fp32 squared norms of the STORED values.
+// fold (MODE 2 storage, FOLD kernels): 1 = base row, stored as -2x with the
+// row's squared norm split exactly into 3 bf16 at columns d..d+2; 2 = query
+// row, with 1.0 at columns d..d+2.  Then <query, base> = xn - 2 q.x.
 template <int MODE>
 __global__ void prep_rows_kernel(const void* __restrict__ x, int in_dtype, int64_t n, int d, int dp,
                                  void* __restrict__ out0, void* __restrict__ out1, float* __restrict__ norms,
-                                 int64_t row0) {
+                                 int64_t row0, int fold) {
   const int64_t rloc = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (rloc >= n) return;
@@ -1016,20 +1071,32 @@ __global__ void prep_rows_kernel(const void* __restrict__ x, int in_dtype, int64
       acc += (double)vr * (double)vr;
     } else {
       const __nv_bfloat16 h = __float2bfloat16_rn(v);
-      static_cast<__nv_bfloat16*>(out0)[(size_t)orow * dp + c] = h;
       const float vr = __bfloat162float(h);
+      if (!(fold && c >= d && c < d + 3))
+        static_cast<__nv_bfloat16*>(out0)[(size_t)orow * dp + c] = (fold == 1) ? __float2bfloat16_rn(-2.f * vr) : h;
       acc += (double)vr * (double)vr;
     }
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, off);
-  if (lane == 0 && norms != nullptr) norms[orow] = static_cast<float>(acc);
+  const float xn = static_cast<float>(acc);
+  if (lane == 0 && norms != nullptr) norms[orow] = xn;
+  if (MODE == 2 && fold && lane < 3) {
+    // xn = h0 + h1 + h2 exactly: each bf16 takes the next 8 significant bits
+    float part = xn, hv = 0.f;
+    for (int i = 0; i <= lane; ++i) {
+      hv = __bfloat162float(__float2bfloat16_rn(part));
+      part -= hv;  // exact (Sterbenz / representable remainder)
+    }
+    static_cast<__nv_bfloat16*>(out0)[(size_t)orow * dp + d + lane] = __float2bfloat16_rn(fold == 1 ? hv : 1.f);
+  }
 }
 
 // Stored rows (by position) back to float32 n x d.
 template <int MODE>
 __global__ void reconstruct_kernel(const void* __restrict__ s0, const void* __restrict__ s1, int dp, int d,
-                                   const int64_t* __restrict__ positions, int64_t n, float* __restrict__ out) {
+                                   const int64_t* __restrict__ positions, int64_t n, float* __restrict__ out,
+                                   float scale) {
   const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (i >= n) return;
@@ -1042,7 +1109,7 @@ __global__ void reconstruct_kernel(const void* __restrict__ s0, const void* __re
       v = __half2float(static_cast<const __half*>(s0)[(size_t)r * dp + c]);
     else
       v = __bfloat162float(static_cast<const __nv_bfloat16*>(s0)[(size_t)r * dp + c]);
-    out[(size_t)i * d + c] = v;
+    out[(size_t)i * d + c] = v * scale;  // scale -0.5 undoes the folded -2x (exact)
   }
 }
 

@@ -201,9 +201,9 @@ class FlatIndex(Index):
         return (ms[0], ms[1], ms[2]), nl.value
 
     def last_plan(self) -> dict:
-        v = (ctypes.c_int * 8)()
+        v = (ctypes.c_int * 12)()  # FK_PLAN_INTS
         N.check(N.lib().fk_last_plan(self._h, v))
-        keys = ("grid", "S", "chunk_tiles", "units", "stages", "a_resident", "smem", "kq")
+        keys = ("grid", "S", "chunk_tiles", "units", "stages", "a_mode", "smem", "kq", "acc_stages", "epi")
         return dict(zip(keys, list(v)))
 
 

@@ -36,23 +36,26 @@ for r in rows[2:]:
     print("  stall samples:", ", ".join(f"{n} {100 * v / tot:.1f}%" for v, n in sorted(st, reverse=True)[:12]))
 
 if "--source" in sys.argv:
+    # hottest SASS instructions by warp-stall samples (with the stall breakdown column)
     n = int(sys.argv[sys.argv.index("--source") + 1])
-    src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda"],
+    src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
     srows = list(csv.reader(io.StringIO(src)))
-    h = srows[0]
-    try:
-        ci = h.index("Warp Stall Sampling (All Samples)")
-    except ValueError:
-        ci = next(i for i, x in enumerate(h) if "Sampling" in x)
-    li = h.index("Line") if "Line" in h else 0
-    si = h.index("Source") if "Source" in h else 1
+    hi = next(i for i, r in enumerate(srows) if r and r[0] == "Address")
+    h = srows[hi]
+    ci = h.index("Warp Stall Sampling (All Samples)")
+    ei = h.index("Instructions Executed")
     body = []
-    for r in srows[1:]:
+    for idx, r in enumerate(srows[hi + 1:]):
         try:
-            body.append((float(r[ci] or 0), r[li], r[si][:110]))
+            body.append((float(r[ci] or 0), idx, float(r[ei] or 0), r[1].strip()[:90]))
         except (ValueError, IndexError):
             pass
     tot = sum(b[0] for b in body) or 1
-    for v, line, s in sorted(body, reverse=True)[:n]:
-        print(f"  {100 * v / tot:5.1f}%  L{line:>5}  {s}")
+    print(f"  {len(body)} SASS instructions; samples%  #idx  warp-instr executed  sass")
+    for v, idx, ex, s in sorted(body, reverse=True)[:n]:
+        print(f"  {100 * v / tot:5.1f}%  #{idx:<6} {ex:14.0f}  {s}")
+    if "--dump" in sys.argv:
+        with open(sys.argv[sys.argv.index("--dump") + 1], "w") as f:
+            for v, idx, ex, s in body:
+                f.write(f"{idx:6d} {100 * v / tot:6.2f}% {ex:12.0f}  {s}\n")

@@ -14,11 +14,22 @@ for kv in os.environ.get("OVERRIDE", "").split(","):
     if kv:
         a, b = kv.split("=")
         cfg[a] = int(b) if b.isdigit() else b
-idx = FlatIndex(cfg["d"], METRIC_L2 if cfg["metric"] == "l2" else METRIC_IP, storage=cfg["storage"])
-for lo in range(0, cfg["nb"], 2_000_000):
-    hi = min(cfg["nb"], lo + 2_000_000)
-    idx.add(torch.from_numpy(gen_base(cfg, lo, hi)).cuda() if cfg["nb"] <= 2_000_000 else gen_base_device(cfg, lo, hi))
-    torch.cuda.empty_cache()
+if os.environ.get("FK_DEV_LIB") == "1":  # FK_DEBUG_FLAGS variants need the FK_DEV build
+    from paper_2401_08281_b200 import build as B
+    B.build(verbose=False, dev=True)
+
+
+def make_index():
+    idx = FlatIndex(cfg["d"], METRIC_L2 if cfg["metric"] == "l2" else METRIC_IP, storage=cfg["storage"])
+    for lo in range(0, cfg["nb"], 2_000_000):
+        hi = min(cfg["nb"], lo + 2_000_000)
+        idx.add(torch.from_numpy(gen_base(cfg, lo, hi)).cuda() if cfg["nb"] <= 2_000_000 else gen_base_device(cfg, lo, hi))
+        torch.cuda.empty_cache()
+    return idx
+
+
+CREATE_TIME = ("FK_NO_FOLD", "FK_NUM_SMS")  # read by fk_create: rebuild the index for these variants
+idx = make_index()
 q = torch.from_numpy(gen_queries(cfg)).cuda()
 variants = [v for v in sys.argv[1:]] or [""]
 ref = None
@@ -26,6 +37,10 @@ for v in variants:
     env = dict(kv.split("=") for kv in v.split(";") if kv)
     for a, b in env.items():
         os.environ[a] = b
+    if any(a in CREATE_TIME for a in env):
+        del idx
+        torch.cuda.empty_cache()
+        idx = make_index()
     for _ in range(3):
         r = idx.search(q, cfg["k"])
     torch.cuda.synchronize()
@@ -52,3 +67,7 @@ for v in variants:
                       "same_as_first": same}), flush=True)
     for a in env:
         del os.environ[a]
+    if any(a in CREATE_TIME for a in env):
+        del idx
+        torch.cuda.empty_cache()
+        idx = make_index()

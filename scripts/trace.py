@@ -1,10 +1,13 @@
 """Per-tile clock64 timeline of CTA 0 (producer/MMA/epilogue handoffs)."""
 import ctypes, os, sys, json
+os.environ["FK_DEV_LIB"] = "1"  # timeline trace lives in the FK_DEV build only
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from bench import CONFIGS, gen_base, gen_queries
 from paper_2401_08281_b200 import FlatIndex, METRIC_L2, METRIC_IP
 from paper_2401_08281_b200 import _native as N
+from paper_2401_08281_b200 import build as B
+B.build(verbose=False, dev=True)
 cfg = dict(CONFIGS[int(os.environ.get("CFG", "2"))])
 for kv in os.environ.get("OVERRIDE", "").split(","):
     if kv:
@@ -31,3 +34,5 @@ print("mma wait tempty", np.median(t[sl, 1] - t[sl, 0]), "| got_tempty->kb0 full
       "| kb1 full->issued", np.median(t[sl, 10] - t[sl, 14]))
 print("epi: commit->got_tfull", np.median(t[sl, 5] - t[sl, 3]), "| busy", np.median(t[sl, 7] - t[sl, 6]),
       "| epi done -> mma got tempty(next use)", np.median(t[22:242, 1] - t[20:240, 7]))
+slow = t[:, 8]
+print("slow-path lanes per tile (warp 0): mean", slow[sl].mean(), "tiles with any", (slow[sl] > 0).mean())

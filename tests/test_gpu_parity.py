@@ -190,8 +190,55 @@ def test_tensor_core_inner_products_vs_fp64():
         assert err < tol, (storage, err)
 
 
+def test_folded_norm_accumulators():
+    """bf16 L2 with free K padding folds the norms into the operands: the raw
+    TMEM accumulator is xn - 2 q.x (base rows stored as -2x | xn split in three
+    bf16, queries as q | 1 1 1).  Exact products, fp32 accumulation."""
+    import ctypes
+    from paper_2401_08281_b200 import _native as N
+    rng = np.random.default_rng(15)
+    xb = rng.standard_normal((700, 96), dtype=np.float32)
+    q = rng.standard_normal((300, 96), dtype=np.float32)
+    qr, xr = O.round_to(q, "bf16").astype(np.float64), O.round_to(xb, "bf16").astype(np.float64)
+    xn = (xr * xr).sum(1).astype(np.float32).astype(np.float64)
+    want = xn[None, :] - 2.0 * (qr @ xr.T)
+    idx = FlatIndex(96, METRIC_L2, storage="bf16")
+    idx.add(xb)
+    buf = torch.zeros((300, 700), dtype=torch.float32, device="cuda")
+    N.check(N.lib().fk_debug_set_ip_dump(idx._h, ctypes.c_void_p(buf.data_ptr())))
+    idx.search(q, 4)
+    N.check(N.lib().fk_debug_set_ip_dump(idx._h, None))
+    got = buf.cpu().numpy().astype(np.float64)
+    scale = xn[None, :] + 2.0 * (np.abs(qr) @ np.abs(xr).T)
+    assert np.max(np.abs(got - want) / scale) < 2e-6
+    # reconstruct undoes the -2x scaling exactly
+    rec = idx.reconstruct_batch(np.arange(50))
+    rec = rec.cpu().numpy() if hasattr(rec, "cpu") else rec
+    assert np.array_equal(rec, xr[:50].astype(np.float32))
+
+
+def test_fold_matches_unfolded_layout():
+    """Same top-k from the folded (MODE 3) and the separate-norm-tile layouts."""
+    rng = np.random.default_rng(16)
+    xb = rng.standard_normal((30000, 96), dtype=np.float32)
+    q = rng.standard_normal((500, 96), dtype=np.float32)
+    res = []
+    for nofold in ("0", "1"):
+        os.environ["FK_NO_FOLD"] = nofold
+        try:
+            idx = FlatIndex(96, METRIC_L2, storage="bf16")
+            idx.add(xb)
+            res.append(idx.search(q, 10))
+        finally:
+            del os.environ["FK_NO_FOLD"]
+    xr, qr = O.round_to(xb, "bf16"), O.round_to(q, "bf16")
+    want_ids, want_dist = O.flat_search_blas(xr, qr, 10, "l2")
+    for r in res:
+        assert_parity(r.ids, r.distances, want_ids, want_dist)
+
+
 PLAN_VARIANTS = [("FK_FORCE_S", "1"), ("FK_FORCE_S", "7"), ("FK_FORCE_S", "64"), ("FK_FORCE_AMODE", "1"),
-                 ("FK_FORCE_AMODE", "2"), ("FK_EPI", "8"), ("FK_STAGES", "2")]
+                 ("FK_FORCE_AMODE", "2"), ("FK_EPI", "8"), ("FK_STAGES", "2"), ("FK_ACC", "2"), ("FK_ACC", "3")]
 
 
 @pytest.mark.parametrize("storage", ["fp32", "bf16"])
