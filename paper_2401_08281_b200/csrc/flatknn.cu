@@ -89,6 +89,8 @@ int make_map(CUtensorMap* m, const void* base, int elem_bytes, uint64_t cols, ui
 }
 
 constexpr int FK_MAX_K = 2048;
+constexpr size_t L2_CHUNK_BYTES = 48ull << 20;  // streamed base per N-chunk (2 chunks in flight << 126 MB L2)
+constexpr size_t PARTIAL_BYTES = 4ull << 30;    // split-N partial top-k lists
 constexpr int MERGE_SMC = 16384;    // large-k merge: survivors gathered in smem (128 KB) + 2048 winners
 constexpr int SMEM_LIMIT = 232448 - 1024;  // sm_100 227 KB per block, minus the static barrier block
 constexpr int SMEM_RESERVE = 1024 /*align*/ + 512 /*barriers + tmem slot*/;
@@ -270,12 +272,15 @@ int launch_fused(int epi, int storage, bool fold, bool ip, int kq, const CUtenso
 // one contiguous range of base tiles).  Units are ordered chunk-major, so the
 // CTAs resident at any moment stream the same ~2 chunks of the base through
 // L2 (the base is read from HBM about once per wave).
-void plan_split(int num_m, int n_tiles, int num_sms, int max_S, int* S_out, int* chunk_out) {
+// min_S bounds a chunk to an L2-resident window (units of one chunk start
+// together; over a long chunk they drift apart and re-read it from HBM);
+// max_S bounds the partial-list memory.
+void plan_split(int num_m, int n_tiles, int num_sms, int min_S, int max_S, int* S_out, int* chunk_out) {
   double best_cost = 1e300;
   int bestS = 1, bestC = n_tiles;
   const double ovh = 1.5;  // per-unit cost in tile-equivalents (A reload, pipeline fill, flush)
-  const int smax = std::min(max_S, n_tiles);
-  for (int S = 1; S <= smax; ++S) {
+  const int smax = std::max(1, std::min(max_S, n_tiles));
+  for (int S = std::max(1, std::min(min_S, smax)); S <= smax; ++S) {
     const int chunk = (n_tiles + S - 1) / S;
     const int s_eff = (n_tiles + chunk - 1) / chunk;
     if (s_eff != S) continue;
@@ -418,23 +423,31 @@ namespace {
 
 struct Plan {
   int kq, epi, nh, num_m, n_tiles, S, chunk_tiles, num_units, grid, a_mode, stages, smem, S_tot, cap, xn_slots,
-      acc_stages;
+      acc_stages, n_issuers;
 };
 
 // Tile / split-N / pipeline plan for one fused pass over base rows [0, nb_pass).
 int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force_S, Plan* pl) {
   Plan P{};
   P.kq = kq;
-  P.epi = 4;
+  // 16-bit storage: 2 epilogue warps per TMEM lane quarter (the epilogue, not
+  // the MMA, paces a 16-bit tile); fp32 3xTF32 is MMA-paced -> 1 per quarter
+  P.epi = h->storage == FK_F32 ? 4 : 8;
   if (const char* e = getenv("FK_EPI")) P.epi = atoi(e) == 8 ? 8 : 4;
   P.nh = P.epi / 4;
   P.num_m = (int)((nq + BM - 1) / BM);
   P.n_tiles = (int)((nb_pass + BN - 1) / BN);
-  plan_split(P.num_m, P.n_tiles, h->num_sms, 128 / P.nh, &P.S, &P.chunk_tiles);
+  // chunk <= L2_CHUNK_BYTES of streamed base; partial lists <= PARTIAL_BYTES
+  const size_t tile_bytes = (size_t)BN * h->dp * elem_bytes_of(h->storage) * split_of(h->storage);
+  const int max_chunk = std::max<int>(64, (int)(L2_CHUNK_BYTES / tile_bytes));
+  const int min_S = (P.n_tiles + max_chunk - 1) / max_chunk;
+  const size_t list_bytes = (size_t)nq * P.nh * std::max(k, 1) * 8;  // one chunk's partial lists
+  const int max_S = (int)std::max<size_t>(1, std::min<size_t>(PARTIAL_BYTES / list_bytes, 1 << 20));
+  plan_split(P.num_m, P.n_tiles, h->num_sms, min_S, max_S, &P.S, &P.chunk_tiles);
   int fs = force_S;
   if (const char* e = getenv("FK_FORCE_S"); e && !force_S) fs = atoi(e);
   if (fs > 0) {
-    P.S = std::max(1, std::min(fs, std::min(128 / P.nh, P.n_tiles)));
+    P.S = std::max(1, std::min(fs, std::min(max_S, P.n_tiles)));
     P.chunk_tiles = (P.n_tiles + P.S - 1) / P.S;
     P.S = (P.n_tiles + P.chunk_tiles - 1) / P.chunk_tiles;
   }
@@ -444,7 +457,11 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   const int num_kb = h->dp / chunk_elems_of(h->storage);
   const int a_bytes = split * num_kb * (int)CHUNK_BYTES;
   const int a_tmem_cols = h->storage == FK_F32 ? 2 * h->dp : h->dp / 2;
+  // Query operand: TMEM (TS MMA) when it leaves room for the accumulator
+  // ring.  With two epilogue groups (16-bit) the ring needs 4 buffers (an even
+  // count, see below), so A moves to smem when it would not leave 4 x 128.
   P.a_mode = a_tmem_cols <= 256 ? 0 : 1;
+  if (P.nh == 2 && a_tmem_cols > 512 - 4 * BN) P.a_mode = 1;
   if (const char* e = getenv("FK_FORCE_AMODE")) P.a_mode = std::max(0, std::min(2, atoi(e)));
   if (P.a_mode == 0 && a_tmem_cols > 256) P.a_mode = 1;
   const int hist_bytes = kq == 0 ? P.epi * 1024 : 0;
@@ -466,6 +483,13 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   // TMEM: 512 columns = acc_stages x 128-column accumulators (+ the query operand in a_mode 0)
   P.acc_stages = std::min(4, (512 - (P.a_mode == 0 ? a_tmem_cols : 0)) / BN);
   if (const char* e = getenv("FK_ACC")) P.acc_stages = std::max(2, std::min(P.acc_stages, atoi(e)));
+  P.n_issuers = P.stages >= 4 ? 2 : 1;  // each issuer needs a sub-ring of >= 2 slots
+  if (const char* e = getenv("FK_ISSUERS")) P.n_issuers = (atoi(e) == 1 || P.stages < 4) ? 1 : 2;
+  // Tiles alternate between the 2 MMA issuers and between the NH epilogue
+  // groups; each party must wait on EVERY phase of the buffers it uses (an
+  // mbarrier parity wait cannot skip a phase), so buffer = tile % acc_stages
+  // must map each party onto its own buffers: acc_stages % parties == 0.
+  if ((P.n_issuers == 2 || P.nh == 2) && (P.acc_stages & 1)) P.acc_stages -= 1;
   P.smem = SMEM_RESERVE + hist_bytes + xn_bytes + (P.a_mode == 1 ? a_bytes : 0) +
            P.stages * (P.a_mode == 2 ? 2 : 1) * split * (int)CHUNK_BYTES;
   P.S_tot = P.S * P.nh;
@@ -528,9 +552,9 @@ int run_fused(fk_index* h, const Plan& P, int64_t nq, int64_t nb_pass, int k, bo
     const int last = h->d + (h->fold ? 3 : 0) - (sp.num_kb - 1) * bk;  // K elements in the last chunk (1..bk)
     sp.kk_last = (last + kstep - 1) / kstep;
   }
-  sp.n_issuers = P.stages >= 4 ? 2 : 1;  // each issuer needs a sub-ring of >= 2 slots
-  if (const char* e = getenv("FK_ISSUERS")) sp.n_issuers = (atoi(e) == 1 || P.stages < 4) ? 1 : 2;
+  sp.n_issuers = P.n_issuers;
   if (const char* e = getenv("FK_DEBUG_FLAGS")) sp.dbg_flags = atoi(e);
+  if (const char* e = getenv("FK_B_POLICY")) sp.b_policy = atoi(e);
   rc = launch_fused(P.epi, h->storage, h->fold != 0, ip, P.kq, ta0, ta1, tb0, tb1, sp, P.grid, P.smem, st);
   if (rc == FK_OK) h->nlaunch++;
   return rc;
@@ -540,7 +564,7 @@ int launch_merge(fk_index* h, const Plan& P, int64_t nq, int k, bool ip, float* 
                  int* fail, cudaStream_t st) {
   const uint32_t* pk = static_cast<const uint32_t*>(h->pkey.p);
   const uint32_t* pp = static_cast<const uint32_t*>(h->ppos.p);
-  if (P.kq == 0) {
+  if (P.kq == 0 || P.S_tot > 128) {  // bounded merge (any number of lists)
     int smc = MERGE_SMC;  // FK_MERGE_SMC (tests): lower the smem fast-path limit to exercise the radix fallback
     if (const char* e = getenv("FK_MERGE_SMC")) smc = std::max(1, std::min(MERGE_SMC, atoi(e)));
     static bool merge_cfg = false;
@@ -551,7 +575,7 @@ int launch_merge(fk_index* h, const Plan& P, int64_t nq, int k, bool ip, float* 
                               (MERGE_SMC + FK_MAX_K) * 8));
       merge_cfg = true;
     }
-    const int* pc = static_cast<const int*>(h->pcnt.p);
+    const int* pc = P.kq == 0 ? static_cast<const int*>(h->pcnt.p) : nullptr;  // queue lists: k entries each
     const uint32_t* thr = static_cast<const uint32_t*>(h->thr.p);
     if (ip)
       merge_large_kernel<true><<<(unsigned)nq, 256, (smc + FK_MAX_K) * 8, st>>>(pk, pp, pc, P.S_tot, (int)nq, k, thr,

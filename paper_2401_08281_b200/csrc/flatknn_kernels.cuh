@@ -68,6 +68,7 @@ struct SearchParams {
   int n_issuers;   // MMA-issuing threads (warps 1 and 3)
   int acc_stages;  // TMEM accumulator buffers (2..4); the query operand (a_mode 0) follows them
   int kk_last;     // MMA K-steps in the last 128-byte K-chunk (trims the zero padding of d)
+  int b_policy;    // L2 eviction policy of the streamed base tiles (0 first, 1 normal, 2 last)
   int dbg_flags;   // bottleneck experiments: 1 = epilogue skips compute, 2 = producer skips TMA
 };
 
@@ -255,8 +256,9 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
   constexpr bool FOLD = (MODE == 3);
   constexpr bool XN_TILE = !IS_IP && !FOLD;
   constexpr uint32_t IDESC = make_idesc(AB_FMT, BM, BN);
-  constexpr int NH = EPI / 4;       // epilogue warps per TMEM lane quarter
-  constexpr int COLS = BN / NH;     // accumulator columns per epilogue warp
+  constexpr int NH = EPI / 4;       // epilogue warp groups (one warp per TMEM lane quarter each)
+  constexpr int NG = NH;            // group g owns the tiles with tcount % NG == g
+  constexpr int PIECE = (NG == 1) ? BN : 64;  // accumulator columns per TMEM load batch
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -305,11 +307,11 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     }
     for (int b = 0; b < (int)acc_stages; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], EPI);
+      mbar_init(&tempty[b], 4);  // the 4 warps of the tile's epilogue group
     }
     for (int x = 0; x < xn_slots; ++x) {
       mbar_init(&xfull[x], 1);
-      mbar_init(&xempty[x], EPI);
+      mbar_init(&xempty[x], 4);
     }
     mbar_init(afull, a_mode == 0 ? EPI : 1);
     mbar_init(aempty, p.n_issuers);
@@ -325,7 +327,9 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     // ===================== TMA producer =====================
     if (lane == 0) {
       const uint64_t pol_a = policy_evict_last();
-      const uint64_t pol_b = policy_evict_first();
+      // streamed base: evict_first by default (FK_B_POLICY=1 normal, 2 last)
+      const uint64_t pol_b = p.b_policy == 2 ? policy_evict_last()
+                             : p.b_policy == 1 ? policy_evict_normal() : policy_evict_first();
       // one FIFO sub-ring of `sh` slots per MMA issuer (tile t -> ring t % nis)
       const uint32_t nis = p.n_issuers;
       const uint32_t sh = (uint32_t)stages / nis;
@@ -494,7 +498,8 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     // ===================== epilogue =====================
     const int ew = warp - EPI_WARP0;
     const int eq = warp & 3;  // TMEM lane quarter this warp may access
-    const int h = ew >> 2;    // column slice of the accumulator
+    const int g = ew >> 2;    // warp group: owns every NG-th tile (and partial list g of each unit)
+    const int h = g;
     const uint32_t lane_addr = static_cast<uint32_t>(eq * 32) << 16;
     const int k = p.k;
     const int dp = num_kb * BK;
@@ -589,6 +594,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         }
       };
 
+      uint32_t own_tiles = 0;  // tiles of this unit processed by this warp group (publish cadence)
       for (int t = t0; t < t1; ++t, ++tcount) {
         const uint32_t buf = a_buf, tph = a_ph;
         if (++a_buf == acc_stages) {
@@ -596,20 +602,21 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
           a_ph ^= 1;
         }
         const uint32_t xslot = x_slot, xph = x_phase;
-        if (++x_slot == (uint32_t)xn_slots) {
+        if (XN_TILE && ++x_slot == (uint32_t)xn_slots) {
           x_slot = 0;
           x_phase ^= 1;
         }
-        const bool tr = FK_DEV && p.trace != nullptr && blockIdx.x == 0 && tcount < 256 && ew == 0 && lane == 0;
+        if (NG > 1 && (tcount & (NG - 1)) != (uint32_t)g) continue;  // another group's tile
+        const bool tr = FK_DEV && p.trace != nullptr && blockIdx.x == 0 && tcount < 256 && eq == 0 && lane == 0;
         if (tr) p.trace[tcount * 16 + 4] = clock64();
         mbar_wait(&tfull[buf], tph);
         if (tr) p.trace[tcount * 16 + 5] = clock64();
         if (XN_TILE) mbar_wait(&xfull[xslot], xph);
         tc_fence_after();
         if (tr) p.trace[tcount * 16 + 6] = clock64();
-        const int n0 = t * BN + h * COLS;
+        const int n0 = t * BN;
         const int nvalid = p.nb - n0;
-        const float* xs = xn_s + xslot * BN + h * COLS;
+        const float* xs = xn_s + xslot * BN;
         // Filter on f = xn - 2 ip (L2; one FMA) or -ip (IP) against T; the
         // exact reference value (qn + xn) - 2 ip is computed for survivors only.
         auto chunk_f = [&](const uint32_t (&r)[32], int c0, float (&f)[32]) {
@@ -661,53 +668,59 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             }
           }
         };
-        // (1) pull this warp's accumulator slice into registers, (2) hand the
-        // TMEM buffer straight back to the MMA issuer, (3) filter + select from
-        // registers while the tensor pipe already fills the buffer again.
+        // Per PIECE of columns: (1) accumulators -> registers; after the last
+        // piece (2) hand the TMEM buffer back to the MMA issuer; (3) filter +
+        // select from registers.  Tiles alternate between warp groups, so a
+        // group has NG tile periods to finish one tile.
         const bool do_epi = !(FK_DEV && (p.dbg_flags & 1));
-        uint32_t racc[COLS];
-        if (do_epi) {
 #pragma unroll
-          for (int c = 0; c < COLS / 32; ++c)
-            tmem_ld_32x32b_x32(tmem_base + lane_addr + buf * BN + h * COLS + c * 32,
-                               *reinterpret_cast<uint32_t(*)[32]>(&racc[32 * c]));
-          tmem_ld_wait();
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[buf]);
-        if (do_epi) {
-          if (p.dbg_ip != nullptr && row_ok) {
-            for (int j = 0; j < COLS; ++j)
-              if (j < nvalid) p.dbg_ip[(size_t)row * p.nb + n0 + j] = __uint_as_float(racc[j]);
-          }
-          // fast path: one straight-line block, a single branch per tile
-          float m = 0.f;
+        for (int pc = 0; pc < BN / PIECE; ++pc) {
+          uint32_t racc[PIECE];
+          if (do_epi) {
 #pragma unroll
-          for (int c = 0; c < COLS / 32; ++c) {
-            float f[32];
-            chunk_f(*reinterpret_cast<const uint32_t(*)[32]>(&racc[32 * c]), c * 32, f);
-            const float mc = IS_IP ? -reduce32<true>(f) : reduce32<false>(f);
-            m = (c == 0) ? mc : fmin_nan(m, mc);
+            for (int c = 0; c < PIECE / 32; ++c)
+              tmem_ld_32x32b_x32(tmem_base + lane_addr + buf * BN + pc * PIECE + c * 32,
+                                 *reinterpret_cast<uint32_t(*)[32]>(&racc[32 * c]));
+            tmem_ld_wait();
           }
-          const bool slow = !(m > T) && row_ok && !(FK_DEV && (p.dbg_flags & 4));
-          if (FK_DEV && p.trace != nullptr) {
-            const unsigned sb = __ballot_sync(FULLMASK, slow);
-            if (tr) p.trace[tcount * 16 + 8] = __popc(sb);
+          if (pc == BN / PIECE - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[buf]);
           }
-          if (slow) {  // divergent, rare
+          if (do_epi) {
+            if (p.dbg_ip != nullptr && row_ok) {
+              for (int j = 0; j < PIECE; ++j)
+                if (pc * PIECE + j < nvalid) p.dbg_ip[(size_t)row * p.nb + n0 + pc * PIECE + j] = __uint_as_float(racc[j]);
+            }
+            // fast path: straight-line min tree, a single branch per piece
+            float m = 0.f;
 #pragma unroll
-            for (int c = 0; c < COLS / 32; ++c)
-              slow_chunk(*reinterpret_cast<const uint32_t(*)[32]>(&racc[32 * c]), c * 32);
+            for (int c = 0; c < PIECE / 32; ++c) {
+              float f[32];
+              chunk_f(*reinterpret_cast<const uint32_t(*)[32]>(&racc[32 * c]), pc * PIECE + c * 32, f);
+              const float mc = IS_IP ? -reduce32<true>(f) : reduce32<false>(f);
+              m = (c == 0) ? mc : fmin_nan(m, mc);
+            }
+            const bool slow = !(m > T) && row_ok && !(FK_DEV && (p.dbg_flags & 4));
+            if (FK_DEV && p.trace != nullptr) {
+              const unsigned sb = __ballot_sync(FULLMASK, slow);
+              if (tr) p.trace[tcount * 16 + 8] += __popc(sb);
+            }
+            if (slow) {  // divergent, rare
+#pragma unroll
+              for (int c = 0; c < PIECE / 32; ++c)
+                slow_chunk(*reinterpret_cast<const uint32_t(*)[32]>(&racc[32 * c]), pc * PIECE + c * 32);
+            }
+            __syncwarp();
+            // warp-uniform: make room for the next piece's candidates per row
+            if constexpr (KQ == 0) compact_lanes(p.cap - PIECE);
           }
-          __syncwarp();
-          // warp-uniform: make room for the next tile's COLS candidates per row
-          if constexpr (KQ == 0) compact_lanes(p.cap - COLS);
         }
         __syncwarp();
         if (tr) p.trace[tcount * 16 + 7] = clock64();
         if (lane == 0 && XN_TILE) mbar_arrive(&xempty[xslot]);
-        if (((t - t0) & 15) == 15 && row_ok) {  // publish own k-th, fetch the shared bound
+        if ((++own_tiles & 15) == 0 && row_ok) {  // publish own k-th, fetch the shared bound
           const uint32_t mine = own_key();
           gkey = min(atomicMin(p.thr_key + row, mine), mine);
           thr = unmonotone(min(mine, gkey));
@@ -941,7 +954,7 @@ __global__ void __launch_bounds__(256) merge_large_kernel(const uint32_t* __rest
   const uint32_t thr = thr_key[q];
   const uint32_t* lk = pkey + (size_t)q * S * k;
   const uint32_t* lp = ppos + (size_t)q * S * k;
-  const int* lc = pcnt + (size_t)q * S;
+  const int* lc = pcnt ? pcnt + (size_t)q * S : nullptr;  // NULL: register-queue lists (k each, sentinel-padded)
   if (tid == 0) {
     count = 0;
     count2 = 0;
@@ -950,20 +963,22 @@ __global__ void __launch_bounds__(256) merge_large_kernel(const uint32_t* __rest
   const int total = S * k;
   auto gload = [&](int e) -> uint64_t {
     const int s = e / k, i = e - s * k;
-    if (i >= lc[s]) return ~0ull;
+    if (lc && i >= lc[s]) return ~0ull;
     const uint32_t key = lk[e];
-    if (key > thr) return ~0ull;
+    if (key > thr || lp[e] == 0xFFFFFFFFu) return ~0ull;
     return (static_cast<uint64_t>(key) << 32) | lp[e];
   };
-  for (int s = tid >> 5; s < S; s += blockDim.x >> 5) {  // warp per list: coalesced
-    const int c = lc[s];
-    for (int i = tid & 31; i < c; i += 32) {
-      const uint32_t key = lk[(size_t)s * k + i];
-      if (key <= thr) {
-        const int idx = atomicAdd(&count, 1);
-        if (idx < smc) sm[idx] = (static_cast<uint64_t>(key) << 32) | lp[(size_t)s * k + i];
-      }
+  for (int e = tid; e < total; e += blockDim.x) {  // the query's S*k block is contiguous: flat, coalesced
+    const uint32_t key = lk[e];
+    if (key > thr) continue;
+    const uint32_t ps = lp[e];
+    if (ps == 0xFFFFFFFFu) continue;
+    if (lc) {
+      const int s = e / k;
+      if (e - s * k >= lc[s]) continue;
     }
+    const int idx = atomicAdd(&count, 1);
+    if (idx < smc) sm[idx] = (static_cast<uint64_t>(key) << 32) | ps;
   }
   __syncthreads();
   const int n = count;

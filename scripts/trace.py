@@ -27,12 +27,15 @@ print("plan", idx.last_plan(), os.environ.get("FK_DEBUG_FLAGS"))
 for i in list(range(100, 106)):
     r = t[i] - t0
     print(i, f"wait_tempty {r[0]} got {r[1]} | kb0 full {r[13]} kb0 issued {r[9]} | kb1 full {r[14]} kb1 issued {r[10]} | commit {r[3]} || epi wait {r[4]} got {r[5]} done {r[7]}")
-sl = slice(20, 240)
-print("period", np.median(np.diff(t[sl, 3])))
-print("mma wait tempty", np.median(t[sl, 1] - t[sl, 0]), "| got_tempty->kb0 full", np.median(t[sl, 13] - t[sl, 1]),
-      "| kb0 full->kb0 issued", np.median(t[sl, 9] - t[sl, 13]), "| kb0 issued->kb1 full", np.median(t[sl, 14] - t[sl, 9]),
-      "| kb1 full->issued", np.median(t[sl, 10] - t[sl, 14]))
-print("epi: commit->got_tfull", np.median(t[sl, 5] - t[sl, 3]), "| busy", np.median(t[sl, 7] - t[sl, 6]),
-      "| epi done -> mma got tempty(next use)", np.median(t[22:242, 1] - t[20:240, 7]))
+sl = slice(40, 240)
+m = lambda a: float(np.median(a))
+c = t[:, 3]
+print("period/tile (commit[t+2]-commit[t])/2:", m((c[42:242] - c[40:240]) / 2))
+print("MMA issuer: tempty wait", m(t[sl, 1] - t[sl, 0]), "| kb0 full wait", m(t[sl, 13] - t[sl, 1]),
+      "| kb0 issue", m(t[sl, 9] - t[sl, 13]), "| kb1 full wait", m(t[sl, 14] - t[sl, 9]),
+      "| kb1 issue", m(t[sl, 10] - t[sl, 14]), "| commit", m(t[sl, 3] - t[sl, 10]),
+      "| idle before next own tile", m(t[42:242, 0] - t[40:240, 3]))
+print("epilogue (warp 4): tfull wait", m(t[sl, 5] - t[sl, 4]), "| commit->got", m(t[sl, 5] - t[sl, 3]),
+      "| busy", m(t[sl, 7] - t[sl, 6]), "| done->next wait", m(t[41:241, 4] - t[40:240, 7]))
 slow = t[:, 8]
-print("slow-path lanes per tile (warp 0): mean", slow[sl].mean(), "tiles with any", (slow[sl] > 0).mean())
+print("slow-path lanes per tile (warp 4): mean", slow[sl].mean(), "tiles with any", (slow[sl] > 0).mean())

@@ -259,6 +259,36 @@ def test_plan_invariance(force, storage):
     assert np.array_equal(base.distances, alt.distances)
 
 
+@pytest.mark.parametrize("storage", ["fp32", "bf16"])
+@pytest.mark.parametrize("data", ["normal", "ints"])
+@pytest.mark.parametrize("k", [1, 10, 32])
+def test_many_chunks_bounded_merge(storage, data, k):
+    """More than 128 split-N lists per query (small L2-resident chunks at large
+    nb): register-queue lists go through the bounded merge; the order must
+    equal the single-list order, ties included (ints: massive exact ties)."""
+    rng = np.random.default_rng(21)
+    if data == "ints":
+        xb = rng.integers(0, 4, size=(40000, 24)).astype(np.float32)
+        q = rng.integers(0, 4, size=(150, 24)).astype(np.float32)
+    else:
+        xb = rng.standard_normal((40000, 24), dtype=np.float32)
+        q = rng.standard_normal((150, 24), dtype=np.float32)
+    idx = FlatIndex(24, METRIC_L2, storage=storage)
+    idx.add(xb)
+    os.environ["FK_FORCE_S"] = "200"
+    try:
+        res = idx.search(q, k)
+        plan = idx.last_plan()
+    finally:
+        del os.environ["FK_FORCE_S"]
+    assert plan["S"] * plan["epi"] // 4 > 128, plan
+    xr, qr = O.round_to(xb, storage), O.round_to(q, storage)
+    want_ids, want_dist = O.flat_search_blas(xr, qr, k, "l2")
+    assert_parity(res.ids, res.distances, want_ids, want_dist)
+    if data == "ints":  # exact integer distances: the order must be identical
+        assert np.array_equal(np.asarray(res.ids), want_ids)
+
+
 # ---------------------------------------------------------------- full size (cfg2 shape)
 @pytest.fixture(scope="module")
 def cfg2_index():
