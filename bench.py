@@ -105,18 +105,38 @@ def gen_queries(cfg):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / throttle reasons sampled during the timed region.
+
+    In-process NVML (nvidia_ml_py) every 50 ms: spawning nvidia-smi inside a
+    short timed region stalls GPU submission while it initialises, so it is
+    only the fallback."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # nvmlClocksEventReason bits
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
 
     def __init__(self, gpu_index):
         self.gpu = gpu_index
         self.proc = None
         self.lines = []
+        self.samples = []  # (sm_mhz, max_mhz, reasons bitmask)
+        self.stop = threading.Event()
+        self.nvml = None
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM)
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
@@ -127,11 +147,28 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _poll(self):
+        P = self.nvml
+        while not self.stop.is_set():
+            try:
+                sm = P.nvmlDeviceGetClockInfo(self.handle, P.NVML_CLOCK_SM)
+                try:
+                    rs = P.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
+                except AttributeError:
+                    rs = P.nvmlDeviceGetCurrentClocksThrottleReasons(self.handle)
+                self.samples.append((float(sm), float(self.max_mhz), int(rs)))
+            except Exception:
+                pass
+            self.stop.wait(0.05)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        self.stop.set()
+        if self.nvml is not None:
+            self.t.join(timeout=2)
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -141,6 +178,12 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, reasons = [], [], set()
+        for a, b, rs in self.samples:
+            sm.append(a)
+            mx.append(b)
+            for bit, nm in self.REASONS.items():
+                if rs & bit:
+                    reasons.add(nm)
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
@@ -157,7 +200,7 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvml" if self.samples else "nvidia-smi"}
 
 
 def cpu_oracle_qps(xb, q, k, metric, nq_sample):
@@ -265,7 +308,6 @@ def run_ours(args, cfg):
         return float(t.item())
 
     clk = ClockSampler(local).__enter__()  # sampling starts before warm-up: covers the whole timed region
-    time.sleep(0.3)
     for _ in range(args.warmup):
         index.search(q_dev, k)
     torch.cuda.synchronize()

@@ -439,7 +439,8 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   P.n_tiles = (int)((nb_pass + BN - 1) / BN);
   // chunk <= L2_CHUNK_BYTES of streamed base; partial lists <= PARTIAL_BYTES
   const size_t tile_bytes = (size_t)BN * h->dp * elem_bytes_of(h->storage) * split_of(h->storage);
-  const int max_chunk = std::max<int>(64, (int)(L2_CHUNK_BYTES / tile_bytes));
+  // (large k: partial lists are k deep, so merge cost grows with S -> 4x window)
+  const int max_chunk = std::max<int>(64, (int)(L2_CHUNK_BYTES * (kq == 0 ? 4 : 1) / tile_bytes));
   const int min_S = (P.n_tiles + max_chunk - 1) / max_chunk;
   const size_t list_bytes = (size_t)nq * P.nh * std::max(k, 1) * 8;  // one chunk's partial lists
   const int max_S = (int)std::max<size_t>(1, std::min<size_t>(PARTIAL_BYTES / list_bytes, 1 << 20));
@@ -565,8 +566,14 @@ int launch_merge(fk_index* h, const Plan& P, int64_t nq, int k, bool ip, float* 
   const uint32_t* pk = static_cast<const uint32_t*>(h->pkey.p);
   const uint32_t* pp = static_cast<const uint32_t*>(h->ppos.p);
   if (P.kq == 0 || P.S_tot > 128) {  // bounded merge (any number of lists)
-    int smc = MERGE_SMC;  // FK_MERGE_SMC (tests): lower the smem fast-path limit to exercise the radix fallback
+    // survivors buffer sized to the expected survivor count (~k..2k, the
+    // radix-select fallback covers overflow) so several CTAs share an SM;
+    // winners: k padded to a power of two for the bitonic sort
+    int smc = std::min(MERGE_SMC, std::max(1024, 4 * k));
     if (const char* e = getenv("FK_MERGE_SMC")) smc = std::max(1, std::min(MERGE_SMC, atoi(e)));
+    int p2 = 1;
+    while (p2 < k) p2 <<= 1;
+    const size_t msmem = (size_t)(smc + p2) * 8;
     static bool merge_cfg = false;
     if (!merge_cfg) {
       CK(cudaFuncSetAttribute(merge_large_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -578,11 +585,11 @@ int launch_merge(fk_index* h, const Plan& P, int64_t nq, int k, bool ip, float* 
     const int* pc = P.kq == 0 ? static_cast<const int*>(h->pcnt.p) : nullptr;  // queue lists: k entries each
     const uint32_t* thr = static_cast<const uint32_t*>(h->thr.p);
     if (ip)
-      merge_large_kernel<true><<<(unsigned)nq, 256, (smc + FK_MAX_K) * 8, st>>>(pk, pp, pc, P.S_tot, (int)nq, k, thr,
-                                                                              h->ids, dD, dI, dP, smc, fail);
+      merge_large_kernel<true><<<(unsigned)nq, 256, msmem, st>>>(pk, pp, pc, P.S_tot, (int)nq, k, thr, h->ids, dD, dI,
+                                                                  dP, smc, fail);
     else
-      merge_large_kernel<false><<<(unsigned)nq, 256, (smc + FK_MAX_K) * 8, st>>>(pk, pp, pc, P.S_tot, (int)nq, k, thr,
-                                                                               h->ids, dD, dI, dP, smc, fail);
+      merge_large_kernel<false><<<(unsigned)nq, 256, msmem, st>>>(pk, pp, pc, P.S_tot, (int)nq, k, thr, h->ids, dD,
+                                                                   dI, dP, smc, fail);
   } else {
     const int wpb = 8;
     const unsigned mgrid = (unsigned)((nq + wpb - 1) / wpb);

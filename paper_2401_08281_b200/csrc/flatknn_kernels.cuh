@@ -676,6 +676,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
 #pragma unroll
         for (int pc = 0; pc < BN / PIECE; ++pc) {
           uint32_t racc[PIECE];
+          if (tr && pc == 0) p.trace[tcount * 16 + 2] = clock64();
           if (do_epi) {
 #pragma unroll
             for (int c = 0; c < PIECE / 32; ++c)
@@ -683,6 +684,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
                                  *reinterpret_cast<uint32_t(*)[32]>(&racc[32 * c]));
             tmem_ld_wait();
           }
+          if (tr && pc < 2) p.trace[tcount * 16 + 11 + pc] = clock64();
           if (pc == BN / PIECE - 1) {
             tc_fence_before();
             __syncwarp();

@@ -37,5 +37,8 @@ print("MMA issuer: tempty wait", m(t[sl, 1] - t[sl, 0]), "| kb0 full wait", m(t[
       "| idle before next own tile", m(t[42:242, 0] - t[40:240, 3]))
 print("epilogue (warp 4): tfull wait", m(t[sl, 5] - t[sl, 4]), "| commit->got", m(t[sl, 5] - t[sl, 3]),
       "| busy", m(t[sl, 7] - t[sl, 6]), "| done->next wait", m(t[41:241, 4] - t[40:240, 7]))
+ev = slice(40, 240, 2)
+print("epilogue group 0: LDTM piece0 latency", m(t[ev, 11] - t[ev, 2]), "| piece0 compute + piece1 LDTM", m(t[ev, 12] - t[ev, 11]),
+      "| piece1 compute + tail", m(t[ev, 7] - t[ev, 12]), "| got tfull -> ld issue", m(t[ev, 2] - t[ev, 6]))
 slow = t[:, 8]
 print("slow-path lanes per tile (warp 4): mean", slow[sl].mean(), "tiles with any", (slow[sl] > 0).mean())
