@@ -346,6 +346,15 @@ def run_ours(args, cfg):
     assert isinstance(r.ids, np.ndarray)
 
     peaks, peaks_kind = load_peaks()
+    # DRAM bytes per fused launch from the committed ncu --set full capture
+    traffic, traffic_src = None, None
+    tp = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            tj = json.load(f)
+        if f"cfg{args.config}" in tj and world == 1:
+            traffic = tj[f"cfg{args.config}"]["traffic_bytes"]
+            traffic_src = tj[f"cfg{args.config}"]["capture"]
     # algorithmic work of one fused launch (local shard): 2*nq*nb_local*d flops
     nb_local = local_index.ntotal
     flops = 2.0 * nq * nb_local * d
@@ -369,7 +378,7 @@ def run_ours(args, cfg):
                                   "NCCL all-gather + merge kernel" if world > 1 else "1 GPU",
                    "plan": plan},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": tc_peak, "unit": "TFLOP/s",
-                     "frac": achieved / tc_peak, "traffic": None,
+                     "frac": achieved / tc_peak, "traffic": traffic, "traffic_source": traffic_src,
                      "kernel": "fused_knn_kernel (tcgen05 GEMM + fused top-k)",
                      "kernel_ms": t_fused, "prep_ms": t_prep, "merge_ms": t_merge,
                      "alg_flops_per_launch": flops, "alg_bytes_per_launch": alg_bytes,
