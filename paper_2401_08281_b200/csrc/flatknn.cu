@@ -74,13 +74,13 @@ PFN_encodeTiled_t get_encode() {
 }
 
 // 2-D row-major [rows][cols] tensor, box = 128 bytes of K x 128 rows, SW128.
-int make_map(CUtensorMap* m, const void* base, int elem_bytes, uint64_t cols, uint64_t rows) {
+int make_map(CUtensorMap* m, const void* base, int elem_bytes, uint64_t cols, uint64_t rows, uint32_t box_rows = 128) {
   PFN_encodeTiled_t enc = get_encode();
   if (!enc) return set_err(FK_E_CUDA, "cuTensorMapEncodeTiled unavailable");
   const CUtensorMapDataType dt = elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT16;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * (cuuint64_t)elem_bytes};
-  cuuint32_t box[2] = {(cuuint32_t)(128 / elem_bytes), 128};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / elem_bytes), box_rows};
   cuuint32_t es[2] = {1, 1};
   CUresult r = enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -219,18 +219,47 @@ int launch_prep(int storage, const void* x, int dtype, int64_t n, int d, int dp,
 
 size_t dtype_bytes(int dtype) { return dtype == FK_F32 ? 4 : 2; }
 
-template <int MODE, int KQ, bool IP, int EPI>
-int launch_fused_t(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0, const CUtensorMap& b1,
-                   const SearchParams& sp, int grid, int smem, cudaStream_t st) {
-  auto kern = fused_knn_kernel<MODE, KQ, IP, EPI>;
+template <int MODE, int KQ, bool IP, int EPI, int TBN>
+int launch_fused_tb(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0, const CUtensorMap& b1,
+                    const SearchParams& sp, int grid, int smem, cudaStream_t st) {
+  auto kern = fused_knn_kernel<MODE, KQ, IP, EPI, TBN>;
   static bool configured = false;  // per instantiation
   if (!configured) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
     configured = true;
   }
-  kern<<<grid, 128 + 32 * EPI, smem, st>>>(a0, a1, b0, b1, sp);
+  if (sp.cluster == 2) {  // CTA pairs sharing base tiles (TMA multicast)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(128 + 32 * EPI);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, kern, a0, a1, b0, b1, sp));
+  } else {
+    kern<<<grid, 128 + 32 * EPI, smem, st>>>(a0, a1, b0, b1, sp);
+  }
   CKL();
   return FK_OK;
+}
+
+// 64-column tiles are instantiated only for each storage's default epilogue
+// width (fp32: 4 warps, 16-bit: 8)
+template <int MODE, int KQ, bool IP, int EPI>
+int launch_fused_t(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0, const CUtensorMap& b1,
+                   const SearchParams& sp, int grid, int smem, cudaStream_t st) {
+  if (sp.bn == 64) {
+    if constexpr ((MODE == 0) == (EPI == 4))
+      return launch_fused_tb<MODE, KQ, IP, EPI, 64>(a0, a1, b0, b1, sp, grid, smem, st);
+    return set_err(FK_E_UNSUPPORTED, "64-column tiles need the default epilogue width");
+  }
+  return launch_fused_tb<MODE, KQ, IP, EPI, 128>(a0, a1, b0, b1, sp, grid, smem, st);
 }
 
 template <int MODE, bool IP, int EPI>
@@ -423,7 +452,7 @@ namespace {
 
 struct Plan {
   int kq, epi, nh, num_m, n_tiles, S, chunk_tiles, num_units, grid, a_mode, stages, smem, S_tot, cap, xn_slots,
-      acc_stages, n_issuers;
+      acc_stages, n_issuers, cluster, num_mu, bn;
 };
 
 // Tile / split-N / pipeline plan for one fused pass over base rows [0, nb_pass).
@@ -436,15 +465,49 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   if (const char* e = getenv("FK_EPI")) P.epi = atoi(e) == 8 ? 8 : 4;
   P.nh = P.epi / 4;
   P.num_m = (int)((nq + BM - 1) / BM);
-  P.n_tiles = (int)((nb_pass + BN - 1) / BN);
+  const int split = split_of(h->storage);
+  const int num_kb = h->dp / chunk_elems_of(h->storage);
+  const int a_bytes = split * num_kb * (int)CHUNK_BYTES;
+  const int a_tmem_cols = h->storage == FK_F32 ? 2 * h->dp : h->dp / 2;
+  // Query operand placement and tile width:
+  //  * 16-bit with two epilogue groups: the accumulator ring wants 4 buffers
+  //    (an even count, see below), so A goes to smem (SS MMA) when it fits;
+  //  * A in TMEM (TS MMA) beside >= 2 x 128 accumulator columns;
+  //  * a large A (up to 384 TMEM columns, e.g. d=768 16-bit) stays in TMEM
+  //    with 64-column tiles (2 x 64 accumulators) rather than re-streaming A;
+  //  * otherwise A in smem, or streamed with every stage (a_mode 2).
+  P.bn = 128;
+  if (h->storage != FK_F32 && P.nh == 2 && a_bytes <= 64 * 1024) P.a_mode = 1;
+  else if (a_tmem_cols <= 256) P.a_mode = 0;
+  else if (a_tmem_cols <= 384) {
+    P.a_mode = 0;
+    P.bn = 64;
+  } else P.a_mode = 1;
+  if (const char* e = getenv("FK_FORCE_AMODE")) P.a_mode = std::max(0, std::min(2, atoi(e)));
+  if (const char* e = getenv("FK_BN")) P.bn = atoi(e) == 64 ? 64 : 128;
+  if (P.a_mode == 0 && a_tmem_cols > 512 - 2 * P.bn) P.a_mode = 1;
+  if (P.a_mode != 0) P.bn = 128;
+  if (P.bn == 64) {  // 64-column kernels exist only for the default epilogue width
+    P.epi = h->storage == FK_F32 ? 4 : 8;
+    P.nh = P.epi / 4;
+  }
+  const int bn = P.bn;
+  const int b_chunk = bn * 128;
+  P.n_tiles = (int)((nb_pass + bn - 1) / bn);
+  // cluster mode (FK_CLUSTER=2): CTA pairs take query tiles 2*mu, 2*mu+1 of
+  // the same chunk and share each base tile (half loaded by each, multicast)
+  P.cluster = 1;
+  if (const char* e = getenv("FK_CLUSTER")) P.cluster = atoi(e) == 2 ? 2 : 1;
+  if (P.num_m < 2 || h->num_sms < 2) P.cluster = 1;
+  P.num_mu = (P.num_m + P.cluster - 1) / P.cluster;
   // chunk <= L2_CHUNK_BYTES of streamed base; partial lists <= PARTIAL_BYTES
-  const size_t tile_bytes = (size_t)BN * h->dp * elem_bytes_of(h->storage) * split_of(h->storage);
-  // (large k: partial lists are k deep, so merge cost grows with S -> 4x window)
-  const int max_chunk = std::max<int>(64, (int)(L2_CHUNK_BYTES * (kq == 0 ? 4 : 1) / tile_bytes));
+  const size_t tile_bytes = (size_t)bn * h->dp * elem_bytes_of(h->storage) * split_of(h->storage);
+  // (very large k: partial lists are k deep, so merge cost grows with S -> 4x window)
+  const int max_chunk = std::max<int>(64, (int)(L2_CHUNK_BYTES * (k >= 512 ? 4 : 1) / tile_bytes));
   const int min_S = (P.n_tiles + max_chunk - 1) / max_chunk;
   const size_t list_bytes = (size_t)nq * P.nh * std::max(k, 1) * 8;  // one chunk's partial lists
   const int max_S = (int)std::max<size_t>(1, std::min<size_t>(PARTIAL_BYTES / list_bytes, 1 << 20));
-  plan_split(P.num_m, P.n_tiles, h->num_sms, min_S, max_S, &P.S, &P.chunk_tiles);
+  plan_split(P.num_mu, P.n_tiles, h->num_sms / P.cluster, min_S, max_S, &P.S, &P.chunk_tiles);
   int fs = force_S;
   if (const char* e = getenv("FK_FORCE_S"); e && !force_S) fs = atoi(e);
   if (fs > 0) {
@@ -452,26 +515,17 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
     P.chunk_tiles = (P.n_tiles + P.S - 1) / P.S;
     P.S = (P.n_tiles + P.chunk_tiles - 1) / P.chunk_tiles;
   }
-  P.num_units = P.num_m * P.S;
-  P.grid = std::min(P.num_units, h->num_sms);
-  const int split = split_of(h->storage);
-  const int num_kb = h->dp / chunk_elems_of(h->storage);
-  const int a_bytes = split * num_kb * (int)CHUNK_BYTES;
-  const int a_tmem_cols = h->storage == FK_F32 ? 2 * h->dp : h->dp / 2;
-  // Query operand: TMEM (TS MMA) when it leaves room for the accumulator
-  // ring.  With two epilogue groups (16-bit) the ring needs 4 buffers (an even
-  // count, see below), so A moves to smem when it would not leave 4 x 128.
-  P.a_mode = a_tmem_cols <= 256 ? 0 : 1;
-  if (P.nh == 2 && a_tmem_cols > 512 - 4 * BN) P.a_mode = 1;
-  if (const char* e = getenv("FK_FORCE_AMODE")) P.a_mode = std::max(0, std::min(2, atoi(e)));
-  if (P.a_mode == 0 && a_tmem_cols > 256) P.a_mode = 1;
+  P.num_units = P.num_mu * P.S;  // per CTA pair in cluster mode
+  P.grid = P.cluster * std::min(P.num_units, h->num_sms / P.cluster);
   const int hist_bytes = kq == 0 ? P.epi * 1024 : 0;
-  // norm-tile ring: 3 slots when smem is tight (fp32), 8 otherwise
-  P.xn_slots = (h->metric == FK_METRIC_IP || h->fold) ? 0 : (h->storage == FK_F32 && P.a_mode != 2) ? 3 : 8;
-  const int xn_bytes = P.xn_slots * BN * 4;
+  // norm-tile ring: 4 slots when smem is tight (fp32), 8 otherwise
+  // (even: one sub-ring per producer/issuer pair)
+  P.xn_slots = (h->metric == FK_METRIC_IP || h->fold) ? 0 : (h->storage == FK_F32 && P.a_mode != 2) ? 4 : 8;
+  const int xn_bytes = P.xn_slots * bn * 4;
+  auto stage_bytes_for = [&](int mode) { return split * b_chunk + (mode == 2 ? split * (int)CHUNK_BYTES : 0); };
   auto stages_for = [&](int mode) {
     const int avail = SMEM_LIMIT - SMEM_RESERVE - hist_bytes - xn_bytes - (mode == 1 ? a_bytes : 0);
-    return avail / ((mode == 2 ? 2 : 1) * split * (int)CHUNK_BYTES);
+    return avail / stage_bytes_for(mode);
   };
   P.stages = stages_for(P.a_mode);
   if (P.a_mode == 1 && P.stages < 3) {
@@ -482,7 +536,7 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   if (const char* e = getenv("FK_STAGES")) P.stages = std::max(2, std::min(P.stages, atoi(e)));
   if (P.stages < 2) return set_err(FK_E_UNSUPPORTED, "pipeline does not fit in shared memory");
   // TMEM: 512 columns = acc_stages x 128-column accumulators (+ the query operand in a_mode 0)
-  P.acc_stages = std::min(4, (512 - (P.a_mode == 0 ? a_tmem_cols : 0)) / BN);
+  P.acc_stages = std::min(4, (512 - (P.a_mode == 0 ? a_tmem_cols : 0)) / bn);
   if (const char* e = getenv("FK_ACC")) P.acc_stages = std::max(2, std::min(P.acc_stages, atoi(e)));
   P.n_issuers = P.stages >= 4 ? 2 : 1;  // each issuer needs a sub-ring of >= 2 slots
   if (const char* e = getenv("FK_ISSUERS")) P.n_issuers = (atoi(e) == 1 || P.stages < 4) ? 1 : 2;
@@ -491,8 +545,7 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   // mbarrier parity wait cannot skip a phase), so buffer = tile % acc_stages
   // must map each party onto its own buffers: acc_stages % parties == 0.
   if ((P.n_issuers == 2 || P.nh == 2) && (P.acc_stages & 1)) P.acc_stages -= 1;
-  P.smem = SMEM_RESERVE + hist_bytes + xn_bytes + (P.a_mode == 1 ? a_bytes : 0) +
-           P.stages * (P.a_mode == 2 ? 2 : 1) * split * (int)CHUNK_BYTES;
+  P.smem = SMEM_RESERVE + hist_bytes + xn_bytes + (P.a_mode == 1 ? a_bytes : 0) + P.stages * stage_bytes_for(P.a_mode);
   P.S_tot = P.S * P.nh;
   P.cap = kq == 0 ? (std::max(2 * k, k + 256) + 31) / 32 * 32 : 0;  // >= k + one tile (128) of slack
   *pl = P;
@@ -512,10 +565,11 @@ int run_fused(fk_index* h, const Plan& P, int64_t nq, int64_t nb_pass, int k, bo
   CUtensorMap ta0, ta1, tb0, tb1;
   const int eb = elem_bytes_of(h->storage);
   if ((rc = make_map(&ta0, h->q0.p, eb, h->dp, nq))) return rc;
-  if ((rc = make_map(&tb0, h->s0, eb, h->dp, nb_pass))) return rc;
+  const uint32_t b_rows = P.cluster == 2 ? P.bn / 2 : P.bn;  // cluster mode: each CTA loads half a tile
+  if ((rc = make_map(&tb0, h->s0, eb, h->dp, nb_pass, b_rows))) return rc;
   if (h->storage == FK_F32) {
     if ((rc = make_map(&ta1, h->q1.p, eb, h->dp, nq))) return rc;
-    if ((rc = make_map(&tb1, h->s1, eb, h->dp, nb_pass))) return rc;
+    if ((rc = make_map(&tb1, h->s1, eb, h->dp, nb_pass, b_rows))) return rc;
   } else {
     ta1 = ta0;
     tb1 = tb0;
@@ -554,6 +608,9 @@ int run_fused(fk_index* h, const Plan& P, int64_t nq, int64_t nb_pass, int k, bo
     sp.kk_last = (last + kstep - 1) / kstep;
   }
   sp.n_issuers = P.n_issuers;
+  sp.cluster = P.cluster;
+  sp.bn = P.bn;
+  sp.num_mu = P.num_mu;
   if (const char* e = getenv("FK_DEBUG_FLAGS")) sp.dbg_flags = atoi(e);
   if (const char* e = getenv("FK_B_POLICY")) sp.b_policy = atoi(e);
   rc = launch_fused(P.epi, h->storage, h->fold != 0, ip, P.kq, ta0, ta1, tb0, tb1, sp, P.grid, P.smem, st);
@@ -713,6 +770,7 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
     h->plan[7] = kq * 100 + pl.epi;
     h->plan[8] = pl.acc_stages;
     h->plan[9] = pl.epi;
+    h->plan[10] = pl.bn;
   }
 
   if (!on_device) {

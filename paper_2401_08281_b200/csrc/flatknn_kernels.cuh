@@ -69,6 +69,9 @@ struct SearchParams {
   int acc_stages;  // TMEM accumulator buffers (2..4); the query operand (a_mode 0) follows them
   int kk_last;     // MMA K-steps in the last 128-byte K-chunk (trims the zero padding of d)
   int b_policy;    // L2 eviction policy of the streamed base tiles (0 first, 1 normal, 2 last)
+  int cluster;     // 1, or 2: CTA pairs share each base tile (each loads half, TMA multicast to both)
+  int num_mu;      // query-tile units per chunk: num_m, or ceil(num_m / 2) pairs in cluster mode
+  int bn;          // base rows per tile (template TBN of the launched kernel)
   int dbg_flags;   // bottleneck experiments: 1 = epilogue skips compute, 2 = producer skips TMA
 };
 
@@ -211,7 +214,7 @@ __device__ __forceinline__ int warp_compact_le(uint64_t* buf, int cnt, uint64_t 
 // a_mode 1: queries resident in smem for the unit
 // a_mode 2: queries streamed with every B stage (large d)
 constexpr int MAX_ACC = 4;      // TMEM accumulator buffers
-constexpr int MAX_STAGES = 16;  // smem operand ring  // TMEM accumulator buffers (runtime p.acc_stages); A operand columns follow them
+constexpr int MAX_STAGES = 32;  // smem operand ring  // TMEM accumulator buffers (runtime p.acc_stages); A operand columns follow them
 
 // NaN-propagating min / max over 32 values with 3-input FMNMX (16 instructions).
 template <bool MAX>
@@ -242,7 +245,7 @@ __device__ __forceinline__ float select32(const float (&s)[32], int j) {
   return (j & 16) ? t2[1] : t2[0];
 }
 
-template <int MODE, int KQ, bool IS_IP, int EPI>
+template <int MODE, int KQ, bool IS_IP, int EPI, int TBN>
 __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     fused_knn_kernel(const __grid_constant__ CUtensorMap tm_a0, const __grid_constant__ CUtensorMap tm_a1,
                      const __grid_constant__ CUtensorMap tm_b0, const __grid_constant__ CUtensorMap tm_b1,
@@ -255,6 +258,10 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
   // the epilogue needs no base-norm tile (FOLD).
   constexpr bool FOLD = (MODE == 3);
   constexpr bool XN_TILE = !IS_IP && !FOLD;
+  // TBN: base rows per tile = accumulator columns (128, or 64 when a large
+  // query operand leaves TMEM room for only 2 x 64 accumulator columns)
+  constexpr int BN = TBN;
+  constexpr uint32_t B_CHUNK = (uint32_t)TBN * 128u;  // one TBN-row x 128-byte K-chunk of the base
   constexpr uint32_t IDESC = make_idesc(AB_FMT, BM, BN);
   constexpr int NH = EPI / 4;       // epilogue warp groups (one warp per TMEM lane quarter each)
   constexpr int NG = NH;            // group g owns the tiles with tcount % NG == g
@@ -269,7 +276,8 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
   const int stages = p.stages;
   const int a_mode = p.a_mode;
   const uint32_t a_bytes = (a_mode == 1) ? SPLIT * num_kb * CHUNK_BYTES : 0u;
-  const uint32_t stage_bytes = (a_mode == 2 ? 2 * SPLIT : SPLIT) * CHUNK_BYTES;
+  // stage = [B hi (| B lo)] (a_mode 2: + [A hi (| A lo)], 128-row chunks)
+  const uint32_t stage_bytes = SPLIT * B_CHUNK + (a_mode == 2 ? SPLIT * CHUNK_BYTES : 0u);
   constexpr uint32_t tmem_cols = 512u;  // 1 CTA per SM: take the whole TMEM
 
   uint8_t* a_region = smem;
@@ -279,18 +287,24 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
   uint32_t* hist_base = reinterpret_cast<uint32_t*>(xn_s + xn_slots * BN);  // large-k: [EPI][256]
   // barriers live in static shared memory: constant addresses, nothing to
   // rematerialise inside the hot loops
-  __shared__ __align__(8) uint64_t bars[60];
+  __shared__ __align__(8) uint64_t bars[92];
   uint64_t* full = bars;         // [MAX_STAGES]
-  uint64_t* empty = bars + 16;   // [MAX_STAGES]
-  uint64_t* tfull = bars + 32;   // [MAX_ACC]
-  uint64_t* tempty = bars + 36;  // [MAX_ACC]
-  uint64_t* xfull = bars + 40;   // [8]
-  uint64_t* xempty = bars + 48;  // [8]
-  uint64_t* afull = bars + 56;
-  uint64_t* aempty = bars + 57;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 58);
+  uint64_t* empty = bars + 32;   // [MAX_STAGES]
+  uint64_t* tfull = bars + 64;   // [MAX_ACC]
+  uint64_t* tempty = bars + 68;  // [MAX_ACC]
+  uint64_t* xfull = bars + 72;   // [8]
+  uint64_t* xempty = bars + 80;  // [8]
+  uint64_t* afull = bars + 88;
+  uint64_t* aempty = bars + 89;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 90);
   const uint32_t acc_stages = p.acc_stages;
   const uint32_t tmem_a_col = acc_stages * BN;
+  // cluster mode: the CTA pair walks the same (chunk, tile) sequence with
+  // query tiles m = 2*mu + crank; each CTA loads half of every base tile and
+  // multicasts it, so a stage is reusable only after BOTH CTAs' MMAs read it
+  const int CL = p.cluster;
+  const uint32_t crank = CL == 2 ? cluster_ctarank() : 0u;
+  const int ublock = blockIdx.x / CL, ugrid = gridDim.x / CL;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_b0);
@@ -303,7 +317,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL);  // one commit from each CTA's MMA issuer
     }
     for (int b = 0; b < (int)acc_stages; ++b) {
       mbar_init(&tfull[b], 1);
@@ -320,12 +334,16 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
   if (warp == 2) tmem_alloc(tmem_slot, tmem_cols);
   tc_fence_before();
   __syncthreads();
+  if (CL == 2) cluster_sync();  // peers' barriers are initialised before any multicast targets them
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
-    // ===================== TMA producer =====================
+  if (warp == 0 || (warp == 2 && p.n_issuers == 2)) {
+    // ===================== TMA producers =====================
+    // One producer per MMA issuer (warp 0 -> ring 0, warp 2 -> ring 1): a
+    // producer blocked on one ring's free slots never stalls the other ring.
     if (lane == 0) {
+      const uint32_t myring = (warp == 0) ? 0u : 1u;
       const uint64_t pol_a = policy_evict_last();
       // streamed base: evict_first by default (FK_B_POLICY=1 normal, 2 last)
       const uint64_t pol_b = p.b_policy == 2 ? policy_evict_last()
@@ -333,15 +351,16 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       // one FIFO sub-ring of `sh` slots per MMA issuer (tile t -> ring t % nis)
       const uint32_t nis = p.n_issuers;
       const uint32_t sh = (uint32_t)stages / nis;
-      uint32_t rs0 = 0, rph0 = 0, rs1 = 0, rph1 = 0;  // sub-ring positions (scalars: no local memory)
+      uint32_t rs = 0, rph = 0;  // position in my sub-ring
+      const uint32_t xh = (uint32_t)xn_slots / nis;  // my norm-tile sub-ring: slots [myring*xh, +xh)
       uint32_t xt = 0, xphase = 0, tc = 0;
       int j = 0;
-      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++j) {
-        const int chunk = u / p.num_m;
-        const int m = u - chunk * p.num_m;
+      for (int u = ublock; u < p.num_units; u += ugrid, ++j) {
+        const int chunk = u / p.num_mu;
+        const int m = (u - chunk * p.num_mu) * CL + (int)crank;
         const int t0 = chunk * p.chunk_tiles;
         const int t1 = min(t0 + p.chunk_tiles, p.n_tiles);
-        if (a_mode == 1) {
+        if (a_mode == 1 && myring == 0) {
           if (j > 0) mbar_wait(aempty, (j - 1) & 1);
           mbar_arrive_expect_tx(afull, a_bytes);
           for (int part = 0; part < SPLIT; ++part)
@@ -351,9 +370,10 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         }
         for (int t = t0; t < t1; ++t, ++tc) {
           const uint32_t ring = (nis == 2) ? (tc & 1) : 0;
-          if (XN_TILE) {  // base norms of this tile -> ring slot (consumed by the epilogue)
-            const uint32_t xs = xt, xph = xphase;
-            if (++xt == (uint32_t)xn_slots) {
+          if (ring != myring) continue;  // the other producer's tile
+          if (XN_TILE) {  // base norms of this tile -> my norm sub-ring (consumed by the epilogue)
+            const uint32_t xs = myring * xh + xt, xph = xphase;
+            if (++xt == xh) {
               xt = 0;
               xphase ^= 1;
             }
@@ -362,8 +382,6 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             bulk_load(xn_s + xs * BN, p.xnorm + (size_t)t * BN, BN * sizeof(float), &xfull[xs]);
           }
           for (int kb = 0; kb < num_kb; ++kb) {
-            uint32_t& rs = ring ? rs1 : rs0;
-            uint32_t& rph = ring ? rph1 : rph0;
             const uint32_t stage = ring * sh + rs, phase = rph;
             if (++rs == sh) {
               rs = 0;
@@ -376,12 +394,20 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             }
             mbar_arrive_expect_tx(&full[stage], stage_bytes);
             uint8_t* sb = st_region + stage * stage_bytes;
-            tma_load_2d(sb, &tm_b0, &full[stage], kb * BK, t * BN, pol_b);
-            if (SPLIT == 2) tma_load_2d(sb + CHUNK_BYTES, &tm_b1, &full[stage], kb * BK, t * BN, pol_b);
-            if (a_mode == 2) {
-              tma_load_2d(sb + SPLIT * CHUNK_BYTES, &tm_a0, &full[stage], kb * BK, m * BM, pol_a);
+            if (CL == 2) {  // my half of the tile's rows (swizzle-atom aligned) to both CTAs
+              const uint32_t hoff = crank * (B_CHUNK / 2);
+              tma_load_2d_mc(sb + hoff, &tm_b0, &full[stage], kb * BK, t * BN + (int)crank * (BN / 2), 0x3, pol_b);
               if (SPLIT == 2)
-                tma_load_2d(sb + 3 * CHUNK_BYTES, &tm_a1, &full[stage], kb * BK, m * BM, pol_a);
+                tma_load_2d_mc(sb + B_CHUNK + hoff, &tm_b1, &full[stage], kb * BK, t * BN + (int)crank * (BN / 2),
+                               0x3, pol_b);
+            } else {
+              tma_load_2d(sb, &tm_b0, &full[stage], kb * BK, t * BN, pol_b);
+              if (SPLIT == 2) tma_load_2d(sb + B_CHUNK, &tm_b1, &full[stage], kb * BK, t * BN, pol_b);
+            }
+            if (a_mode == 2) {
+              tma_load_2d(sb + SPLIT * B_CHUNK, &tm_a0, &full[stage], kb * BK, m * BM, pol_a);
+              if (SPLIT == 2)
+                tma_load_2d(sb + SPLIT * B_CHUNK + CHUNK_BYTES, &tm_a1, &full[stage], kb * BK, m * BM, pol_a);
             }
           }
         }
@@ -405,8 +431,8 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       const uint64_t st_desc0 = smem_desc_sw128(smem_u32(st_region));
       const uint64_t a_desc0 = smem_desc_sw128(smem_u32(a_region));
       const int kk_last = p.kk_last;
-      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++j) {
-        const int chunk = u / p.num_m;
+      for (int u = ublock; u < p.num_units; u += ugrid, ++j) {
+        const int chunk = u / p.num_mu;
         const int t0 = chunk * p.chunk_tiles;
         const int t1 = min(t0 + p.chunk_tiles, p.n_tiles);
         if (a_mode != 2) {
@@ -438,7 +464,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             if (tr && kb < 4) p.trace[tcount * 16 + 13 + (kb < 3 ? kb : 2)] = clock64();
             // descriptor start address is in 16-byte units (bits 0-13)
             const uint64_t bd0 = st_desc0 + ((stage * stage_bytes) >> 4);
-            const uint64_t bd1 = bd0 + (CHUNK_BYTES >> 4);
+            const uint64_t bd1 = bd0 + (B_CHUNK >> 4);
             if (elect_one()) {
               if (a_mode == 0) {
                 const uint32_t ah = a_tm + kb * 32;
@@ -459,10 +485,11 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
                   }
                 }
               } else {
-                const uint64_t ad0 = (a_mode == 1) ? a_desc0 + ((kb * CHUNK_BYTES) >> 4) : bd0 + ((SPLIT * CHUNK_BYTES) >> 4);
+                const uint64_t ad0 =
+                    (a_mode == 1) ? a_desc0 + ((kb * CHUNK_BYTES) >> 4) : bd0 + ((SPLIT * B_CHUNK) >> 4);
                 if (MODE == 0) {
                   const uint64_t ad1 = (a_mode == 1) ? a_desc0 + (((num_kb + kb) * CHUNK_BYTES) >> 4)
-                                                     : bd0 + ((3 * CHUNK_BYTES) >> 4);
+                                                     : bd0 + ((2 * B_CHUNK + CHUNK_BYTES) >> 4);
 #pragma unroll
                   for (int kk = 0; kk < 4; ++kk) {
                     if (kk >= nkk) break;
@@ -479,7 +506,8 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
                   }
                 }
               }
-              mma_commit(&empty[stage]);
+              if (CL == 2) mma_commit_mc(&empty[stage], 0x3);  // frees the stage in both CTAs
+              else mma_commit(&empty[stage]);
             }
             __syncwarp();
             if (tr && kb < 4) p.trace[tcount * 16 + 9 + kb] = clock64();
@@ -504,10 +532,12 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     const int k = p.k;
     const int dp = num_kb * BK;
     const int a_cols = (MODE == 0) ? 2 * dp : dp / 2;  // TMEM columns of the query operand
-    uint32_t tcount = 0, x_slot = 0, x_phase = 0, a_buf = 0, a_ph = 0;
-    for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
-      const int chunk = u / p.num_m;
-      const int m = u - chunk * p.num_m;
+    uint32_t tcount = 0, a_buf = 0, a_ph = 0;
+    uint32_t xs0 = 0, xp0 = 0, xs1 = 0, xp1 = 0;  // norm sub-ring positions (ring = tile % n_issuers)
+    const uint32_t xh = (uint32_t)xn_slots / (uint32_t)p.n_issuers;
+    for (int u = ublock; u < p.num_units; u += ugrid) {
+      const int chunk = u / p.num_mu;
+      const int m = (u - chunk * p.num_mu) * CL + (int)crank;
       const int t0 = chunk * p.chunk_tiles;
       const int t1 = min(t0 + p.chunk_tiles, p.n_tiles);
       const int row = m * BM + eq * 32 + lane;
@@ -601,10 +631,17 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
           a_buf = 0;
           a_ph ^= 1;
         }
-        const uint32_t xslot = x_slot, xph = x_phase;
-        if (XN_TILE && ++x_slot == (uint32_t)xn_slots) {
-          x_slot = 0;
-          x_phase ^= 1;
+        uint32_t xslot = 0, xph = 0;
+        if (XN_TILE) {
+          const uint32_t ring = (p.n_issuers == 2) ? (tcount & 1) : 0;
+          uint32_t& xs = ring ? xs1 : xs0;
+          uint32_t& xp = ring ? xp1 : xp0;
+          xslot = ring * xh + xs;
+          xph = xp;
+          if (++xs == xh) {
+            xs = 0;
+            xp ^= 1;
+          }
         }
         if (NG > 1 && (tcount & (NG - 1)) != (uint32_t)g) continue;  // another group's tile
         const bool tr = FK_DEV && p.trace != nullptr && blockIdx.x == 0 && tcount < 256 && eq == 0 && lane == 0;
@@ -759,6 +796,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
 
   tc_fence_before();
   __syncthreads();
+  if (CL == 2) cluster_sync();  // no CTA leaves while its peer may still multicast into it
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, tmem_cols);
