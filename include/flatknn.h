@@ -113,6 +113,18 @@ const char* fk_last_error(void);
 int fk_set_profiling(fk_index* h, int on);
 int fk_kernel_times(fk_index* h, float* ms3, int* nlaunch);
 
+/* k-means assignment in fp64 (replaces annkit quantize.py:38-62 `_assign`,
+ * the Lloyd-iteration / IVF-training consumer of the flat path).
+ * Device pointers: x [n][d] f32, c [nc][d] f64, cnorm [nc] f64, optional
+ * cand [n][kc] (candidate centroid ids per row, e.g. the GPU flat-search
+ * shortlist; NULL = ids 0..kc-1) and approx [n][kc] (their fp32 distances,
+ * best first) -> assign [n] i64, err [n] f64 (max(|x|^2 + |c|^2 - 2 x.c, 0)),
+ * uncertain [n] (1 = shortlist gap below margin*(|x|^2 + cmax): rescore the
+ * row over all centroids).  by_ip: argmax inner product (spherical). */
+int fk_kmeans_rescore(const float* x, int64_t n, int d, const double* c, const double* cnorm, int64_t nc,
+                      const int64_t* cand, int kc, int by_ip, const float* approx, double margin, double cmax,
+                      int64_t* assign, double* err, int* uncertain, void* stream);
+
 /* Tuning / introspection of the last search plan, FK_PLAN_INTS ints: grid,
  * N-chunks (split-N), tiles per chunk, work units, smem pipeline stages,
  * query-operand mode, dynamic smem bytes, 100*queue+epilogue warps, TMEM

@@ -10,6 +10,7 @@ top-k) behind the C ABI declared in ``include/flatknn.h``.
 from .core import (METRIC_IP, METRIC_L2, Index, Metric, MetricKind, SearchResult, as_vectors,
                    knn_recall)
 from .flat import FlatIndex, IndexFlatIP, IndexFlatL2
+from .kmeans import assign_vectors, coarse_quantizer, kmeans_assign, probe_lists
 from .sharded import ShardedFlatIndex
 
 __version__ = "0.1.0"
@@ -26,5 +27,9 @@ __all__ = [
     "SearchResult",
     "ShardedFlatIndex",
     "as_vectors",
+    "assign_vectors",
+    "coarse_quantizer",
+    "kmeans_assign",
     "knn_recall",
+    "probe_lists",
 ]

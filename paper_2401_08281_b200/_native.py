@@ -27,7 +27,7 @@ FK_E_NOTFOUND = -5
 EXPORTED = (
     "fk_create", "fk_add", "fk_search", "fk_merge_shards", "fk_reconstruct", "fk_remove_ids",
     "fk_reset", "fk_ntotal", "fk_dim", "fk_get_ids", "fk_destroy", "fk_last_error",
-    "fk_set_profiling", "fk_kernel_times", "fk_last_plan",
+    "fk_set_profiling", "fk_kernel_times", "fk_last_plan", "fk_kmeans_rescore",
 )
 
 _lib = None
@@ -52,6 +52,8 @@ _SIGS = {
     "fk_set_profiling": (_INT, [_P, _INT]),
     "fk_kernel_times": (_INT, [_P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(_INT)]),
     "fk_last_plan": (_INT, [_P, ctypes.POINTER(_INT)]),
+    "fk_kmeans_rescore": (_INT, [_P, _I64, _INT, _P, _P, _I64, _P, _INT, _INT, _P, ctypes.c_double,
+                                 ctypes.c_double, _P, _P, _P, _P]),
     "fk_debug_set_ip_dump": (_INT, [_P, _P]),
     "fk_debug_set_trace": (_INT, [_P, _P]),
 }

@@ -915,6 +915,20 @@ int fk_kernel_times(fk_index* h, float* ms3, int* nlaunch) {
   return FK_OK;
 }
 
+int fk_kmeans_rescore(const float* x, int64_t n, int d, const double* c, const double* cnorm, int64_t nc,
+                      const int64_t* cand, int kc, int by_ip, const float* approx, double margin, double cmax,
+                      int64_t* assign, double* err, int* uncertain, void* stream) {
+  if (n < 0 || d < 1 || nc < 1 || kc < 1) return set_err(FK_E_INVALID, "bad sizes");
+  if (!x || !c || !cnorm || !assign || !err) return set_err(FK_E_INVALID, "NULL argument");
+  if (n == 0) return FK_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int wpb = 8;
+  kmeans_rescore_kernel<<<(unsigned)((n + wpb - 1) / wpb), wpb * 32, 0, st>>>(
+      x, n, d, c, cnorm, nc, cand, kc, by_ip, approx, margin, cmax, assign, err, uncertain);
+  CKL();
+  return FK_OK;
+}
+
 int fk_last_plan(fk_index* h, int* out) {
   if (!h || !out) return set_err(FK_E_INVALID, "NULL argument");
   std::memcpy(out, h->plan, sizeof(h->plan));

@@ -1204,4 +1204,63 @@ __global__ void fill_sentinel_kernel(float* D, int64_t* I, int64_t* P, size_t n,
   }
 }
 
+// ------------------------------------------------------------ k-means assignment (fp64)
+// Reference quantize.py:38-62 (_assign): nearest centroid in fp64,
+// L2: argmin(cnorm - 2 ip), IP: argmax(ip), first index wins ties; the error
+// is max(xnorm + cnorm[a] - 2 ip[a], 0).  One warp per row evaluates `kc`
+// candidate centroids (the fp32 GPU shortlist, or every centroid) in fp64.
+// With `approx` (the shortlist's fp32 distances, best first) a row is flagged
+// uncertain when the shortlist's first and last values are closer than the
+// fp32 error bound `margin * (xnorm + cmax)`: the true best might then lie
+// outside the shortlist, and the caller rescores that row over all centroids.
+__global__ void kmeans_rescore_kernel(const float* __restrict__ x, int64_t n, int d, const double* __restrict__ c,
+                                      const double* __restrict__ cnorm, int64_t nc, const int64_t* __restrict__ cand,
+                                      int kc, int by_ip, const float* __restrict__ approx, double margin, double cmax,
+                                      int64_t* __restrict__ assign, double* __restrict__ err,
+                                      int* __restrict__ uncertain) {
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const float* xr = x + (size_t)row * d;
+  double xn = 0.0;
+  for (int i = lane; i < d; i += 32) xn += (double)xr[i] * (double)xr[i];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) xn += __shfl_xor_sync(FULLMASK, xn, off);
+  int64_t best = -1;
+  double bval = 0.0, bip = 0.0;
+  for (int j = 0; j < kc; ++j) {
+    const int64_t cj = cand ? cand[(size_t)row * kc + j] : j;
+    if (cj < 0 || cj >= nc) continue;
+    const double* cr = c + (size_t)cj * d;
+    double ip = 0.0;
+    for (int i = lane; i < d; i += 32) ip = fma((double)xr[i], cr[i], ip);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) ip += __shfl_xor_sync(FULLMASK, ip, off);
+    const double v = by_ip ? ip : cnorm[cj] - 2.0 * ip;
+    const bool better = best < 0 || (by_ip ? (v > bval || (v == bval && cj < best))
+                                           : (v < bval || (v == bval && cj < best)));
+    if (better) {
+      best = cj;
+      bval = v;
+      bip = ip;
+    }
+  }
+  if (lane == 0) {
+    assign[row] = best;
+    const double e = best >= 0 ? xn + cnorm[best] - 2.0 * bip : 0.0;
+    err[row] = e > 0.0 ? e : 0.0;  // np.maximum(err, 0.0)
+    if (uncertain) {
+      int u = 0;
+      if (approx && kc > 1) {
+        const float a0 = approx[(size_t)row * kc], a1 = approx[(size_t)row * kc + kc - 1];
+        const double gap = by_ip ? (double)a0 - (double)a1 : (double)a1 - (double)a0;
+        u = !(gap > margin * (xn + cmax));  // NaN-safe: NaN gap -> uncertain
+      } else if (approx) {
+        u = 1;  // a one-entry shortlist cannot be certified
+      }
+      uncertain[row] = u;
+    }
+  }
+}
+
 }  // namespace fk
