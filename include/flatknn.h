@@ -113,6 +113,17 @@ const char* fk_last_error(void);
 int fk_set_profiling(fk_index* h, int on);
 int fk_kernel_times(fk_index* h, float* ms3, int* nlaunch);
 
+/* Range search (replaces annkit flat.py:121-144 `flat_range_search`, reached
+ * through Index.range_search core.py:152-155 / FlatIndex._range_search):
+ * every stored vector with direct distance <= radius (L2) or inner product
+ * >= radius (IP), per query sorted best first with ties by smaller id
+ * (flat.py:137).  Writes lims [nq + 1] (CSR offsets, host or device) and the
+ * entry count to *total; the entries stay in the handle until
+ * fk_range_fetch copies ids [total] (int64) and distances [total] (f32). */
+int fk_range_search(fk_index* h, const void* q, int64_t nq, int dtype, float radius, int64_t* lims, int64_t* total,
+                    int on_device, void* stream);
+int fk_range_fetch(fk_index* h, int64_t* ids, float* dist, int on_device, void* stream);
+
 /* k-means assignment in fp64 (replaces annkit quantize.py:38-62 `_assign`,
  * the Lloyd-iteration / IVF-training consumer of the flat path).
  * Device pointers: x [n][d] f32, c [nc][d] f64, cnorm [nc] f64, optional

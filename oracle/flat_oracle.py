@@ -15,6 +15,8 @@ It restates, in plain numpy, the reference annkit BLAS search path
                            ``(qn + xn) - 2 ip`` in f32, clamp at 0, top-k)
 * ``finish``            <- ``pkg/src/annkit/flat.py:68-73`` (position -> id)
 * ``knn_recall``        <- ``pkg/src/annkit/core.py:314-327``
+* ``flat_range_search`` <- ``pkg/src/annkit/flat.py:121-144`` (direct pairwise
+                           distances, <= radius / >= for IP, (value, id) order)
 
 Parity pinning: ``tests/test_oracle.py`` checks this restatement against the
 golden vectors in ``tests/golden/`` that ``tests/golden/make_golden.py``
@@ -174,3 +176,44 @@ def round_to(x: np.ndarray, storage: str) -> np.ndarray:
         out[nan] = (x.view(np.uint32)[nan] | 0x00400000) & 0xFFFF0000
         return out.view(np.float32)
     return x
+
+
+def direct_distances(q: np.ndarray, xb: np.ndarray, metric: str = METRIC_L2) -> np.ndarray:
+    """core.py:184-188 pairwise_distances -> _kernels.pairwise (per-pair direct
+    loops, _ckernels.pyx:49-57): L2 sum (q - x)^2, IP sum q x.  Accumulated in
+    fp64 and rounded once to fp32 (the reference's fp32 loops differ by ulps)."""
+    q64, x64 = q.astype(np.float64), xb.astype(np.float64)
+    if metric == METRIC_IP:
+        return (q64 @ x64.T).astype(np.float32)
+    d = (q64 * q64).sum(1)[:, None] + (x64 * x64).sum(1)[None, :] - 2.0 * (q64 @ x64.T)
+    # exact-enough for the small oracle cases; recompute the near-zero entries directly
+    small = np.abs(d) < 1e-3 * ((q64 * q64).sum(1)[:, None] + (x64 * x64).sum(1)[None, :] + 1e-30)
+    if small.any():
+        ii, jj = np.nonzero(small)
+        d[ii, jj] = ((q64[ii] - x64[jj]) ** 2).sum(1)
+    return np.maximum(d, 0.0).astype(np.float32)
+
+
+def flat_range_search(xb: np.ndarray, q: np.ndarray, radius: float, metric: str = METRIC_L2,
+                      ids: np.ndarray | None = None):
+    """flat.py:121-144: (lims, ids, distances) with every stored vector within
+    the radius (<= for distances, >= for IP), best first, ties by smaller id."""
+    ids_table = np.arange(xb.shape[0], dtype=np.int64) if ids is None else ids
+    nq = q.shape[0]
+    lims = np.zeros(nq + 1, dtype=np.int64)
+    out_i, out_d = [], []
+    desc = metric == METRIC_IP
+    dmat = direct_distances(q, xb, metric) if xb.shape[0] else np.zeros((nq, 0), np.float32)
+    for r in range(nq):
+        row = dmat[r]
+        mask = row >= radius if desc else row <= radius
+        pos = np.nonzero(mask)[0]
+        vals = row[pos]
+        order = np.lexsort((ids_table[pos], -vals if desc else vals))
+        out_i.append(ids_table[pos][order])
+        out_d.append(vals[order])
+        lims[r + 1] = len(pos)
+    np.cumsum(lims, out=lims)
+    cat_i = np.concatenate(out_i) if out_i else np.empty(0, np.int64)
+    cat_d = np.concatenate(out_d) if out_d else np.empty(0, np.float32)
+    return lims, cat_i, cat_d.astype(np.float32)

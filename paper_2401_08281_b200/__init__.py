@@ -7,7 +7,7 @@ The compute runs in hand-written sm_100a kernels (tcgen05 GEMM + fused
 top-k) behind the C ABI declared in ``include/flatknn.h``.
 """
 
-from .core import (METRIC_IP, METRIC_L2, Index, Metric, MetricKind, SearchResult, as_vectors,
+from .core import (METRIC_IP, METRIC_L2, Index, Metric, MetricKind, RangeResult, SearchResult, as_vectors,
                    knn_recall)
 from .flat import FlatIndex, IndexFlatIP, IndexFlatL2
 from .kmeans import assign_vectors, coarse_quantizer, kmeans_assign, probe_lists
@@ -24,6 +24,7 @@ __all__ = [
     "MetricKind",
     "METRIC_IP",
     "METRIC_L2",
+    "RangeResult",
     "SearchResult",
     "ShardedFlatIndex",
     "as_vectors",

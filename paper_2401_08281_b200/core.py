@@ -140,6 +140,25 @@ class SearchResult:
         yield self.ids
 
 
+@dataclass
+class RangeResult:
+    """Variable-length per-query results in CSR form (core.py:86-104): query i
+    owns entries lims[i]:lims[i+1], each list sorted best first."""
+
+    lims: Any  # (nq + 1,) int64
+    ids: Any  # int64
+    distances: Any  # float32
+    radius: float
+
+    @property
+    def nq(self) -> int:
+        return len(self.lims) - 1
+
+    def row(self, i: int):
+        lo, hi = int(self.lims[i]), int(self.lims[i + 1])
+        return self.ids[lo:hi], self.distances[lo:hi]
+
+
 class Index:
     """Base contract (core.py:107-173): subclasses override the private hooks.
 

@@ -22,6 +22,10 @@
 #include "../../include/flatknn.h"
 #include "flatknn_kernels.cuh"
 
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+
 using namespace fk;
 
 namespace {
@@ -133,6 +137,12 @@ struct fk_index {
   float* xn_max = nullptr;   // device scalar: max stored norm
   int64_t* ids = nullptr;    // [cap]
   DevBuf q_in, q0, q1, qn, pkey, ppos, thr, pcnt, cbuf, fail, outD, outI, outP, stage_in, stage_ids;
+  // range search: candidates, exact pass, sort scratch and the CSR result
+  DevBuf rcand, rcount, rdist, rkid, rkrd, rkeep, rrowc, rsel, rnsel, rtmp, rkid2, rkrd2, rv1, rv2, rlims, rids,
+      rdist_out;
+  float r_radius = 0.f;
+  int64_t r_total = 0, r_nq = 0;
+  unsigned long long r_cap = 0;
   long long est_fallbacks = 0;  // large-k searches whose estimated bound failed certification
   std::mutex mu;
   int num_sms = 148;
@@ -270,6 +280,9 @@ int launch_fused_k(int kq, const CUtensorMap& a0, const CUtensorMap& a1, const C
     case 16: return launch_fused_t<MODE, 16, IP, EPI>(a0, a1, b0, b1, sp, grid, smem, st);
     case 32: return launch_fused_t<MODE, 32, IP, EPI>(a0, a1, b0, b1, sp, grid, smem, st);
     case 0: return launch_fused_t<MODE, 0, IP, EPI>(a0, a1, b0, b1, sp, grid, smem, st);
+    case -1:  // range search: default epilogue width only
+      if constexpr ((MODE == 0) == (EPI == 4)) return launch_fused_t<MODE, -1, IP, EPI>(a0, a1, b0, b1, sp, grid, smem, st);
+      return set_err(FK_E_UNSUPPORTED, "range search runs with the default epilogue width");
   }
   return set_err(FK_E_UNSUPPORTED, "queue bucket %d", kq);
 }
@@ -462,7 +475,7 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   // 16-bit storage: 2 epilogue warps per TMEM lane quarter (the epilogue, not
   // the MMA, paces a 16-bit tile); fp32 3xTF32 is MMA-paced -> 1 per quarter
   P.epi = h->storage == FK_F32 ? 4 : 8;
-  if (const char* e = getenv("FK_EPI")) P.epi = atoi(e) == 8 ? 8 : 4;
+  if (const char* e = getenv("FK_EPI"); e && kq >= 0) P.epi = atoi(e) == 8 ? 8 : 4;
   P.nh = P.epi / 4;
   P.num_m = (int)((nq + BM - 1) / BM);
   const int split = split_of(h->storage);
@@ -610,6 +623,10 @@ int run_fused(fk_index* h, const Plan& P, int64_t nq, int64_t nb_pass, int k, bo
   sp.n_issuers = P.n_issuers;
   sp.cluster = P.cluster;
   sp.bn = P.bn;
+  sp.radius = h->r_radius;
+  sp.rcand = static_cast<unsigned long long*>(h->rcand.p);
+  sp.rcount = static_cast<unsigned long long*>(h->rcount.p);
+  sp.rcap = h->r_cap;
   sp.num_mu = P.num_mu;
   if (const char* e = getenv("FK_DEBUG_FLAGS")) sp.dbg_flags = atoi(e);
   if (const char* e = getenv("FK_B_POLICY")) sp.b_policy = atoi(e);
@@ -660,9 +677,186 @@ int launch_merge(fk_index* h, const Plan& P, int64_t nq, int k, bool ip, float* 
   return FK_OK;
 }
 
+// Queries -> device operand layout + norms (shared by search and range search).
+int stage_queries(fk_index* h, const void* q, int64_t nq, int dtype, int on_device, cudaStream_t st) {
+  int rc;
+  const size_t in_row = (size_t)h->d * dtype_bytes(dtype);
+  const void* qsrc = q;
+  if (!on_device) {
+    if ((rc = h->q_in.ensure(nq * in_row))) return rc;
+    CK(cudaMemcpyAsync(h->q_in.p, q, nq * in_row, cudaMemcpyHostToDevice, st));
+    qsrc = h->q_in.p;
+  }
+  const size_t qrow = row_bytes(h);
+  if ((rc = h->q0.ensure(nq * qrow))) return rc;
+  if (h->storage == FK_F32 && (rc = h->q1.ensure(nq * qrow))) return rc;
+  if ((rc = h->qn.ensure(nq * sizeof(float)))) return rc;
+  return launch_prep(h->storage, qsrc, dtype, nq, h->d, h->dp, h->q0.p, h->q1.p, static_cast<float*>(h->qn.p), 0, st,
+                     h->fold ? 2 : 0);
+}
+
+__global__ void gather_range_kernel(const unsigned int* __restrict__ order, const unsigned long long* __restrict__ key_id,
+                                    const float* __restrict__ dist, int64_t n, int64_t* __restrict__ ids_out,
+                                    float* __restrict__ dist_out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const unsigned int j = order[i];
+    ids_out[i] = static_cast<int64_t>(key_id[j]);
+    dist_out[i] = dist[j];
+  }
+}
+__global__ void gather_u64_kernel(const unsigned int* __restrict__ idx, const unsigned long long* __restrict__ src,
+                                  int64_t n, unsigned long long* __restrict__ dst) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[idx[i]];
+}
+__global__ void iota_u32_kernel(unsigned int* out, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (unsigned int)i;
+}
+__global__ void counts_to_i64_kernel(const unsigned int* __restrict__ c, int64_t nq, int64_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i <= nq) out[i] = i < nq ? (int64_t)c[i] : 0;
+}
+
 }  // namespace
 
 extern "C" {
+
+int fk_range_search(fk_index* h, const void* q, int64_t nq, int dtype, float radius, int64_t* lims, int64_t* total,
+                    int on_device, void* stream) {
+  if (!h) return set_err(FK_E_INVALID, "NULL index");
+  if (nq < 0) return set_err(FK_E_INVALID, "nq must be >= 0");
+  if (dtype != FK_F32 && dtype != FK_F16 && dtype != FK_BF16) return set_err(FK_E_INVALID, "bad dtype %d", dtype);
+  if (!lims || !total) return set_err(FK_E_INVALID, "NULL output pointer");
+  if (nq > (int64_t)INT32_MAX / 2) return set_err(FK_E_UNSUPPORTED, "nq too large for one call");
+  if (nq > 0 && !q) return set_err(FK_E_INVALID, "NULL query pointer");
+  std::lock_guard<std::mutex> g(h->mu);
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool ip = h->metric == FK_METRIC_IP;
+  int rc;
+  h->r_total = 0;
+  h->r_nq = nq;
+  if ((rc = h->rlims.ensure((size_t)(nq + 1) * sizeof(int64_t)))) return rc;
+  int64_t* dlims = static_cast<int64_t*>(h->rlims.p);
+  if (nq == 0 || h->ntotal == 0) {  // flat.py:124-125: empty lists
+    CK(cudaMemsetAsync(dlims, 0, (size_t)(nq + 1) * sizeof(int64_t), st));
+  } else {
+    if ((rc = stage_queries(h, q, nq, dtype, on_device, st))) return rc;
+    Plan pl;
+    if ((rc = make_plan(h, nq, h->ntotal, 1, -1, 0, &pl))) return rc;
+    h->r_radius = radius;
+    if ((rc = h->thr.ensure((size_t)nq * sizeof(uint32_t)))) return rc;
+    if ((rc = h->rcount.ensure(sizeof(unsigned long long)))) return rc;
+    unsigned long long want = std::max<unsigned long long>(h->r_cap, std::max<int64_t>(1 << 20, nq * 64));
+    unsigned long long n = 0;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      if ((rc = h->rcand.ensure(want * sizeof(unsigned long long)))) return rc;
+      h->r_cap = want;
+      CK(cudaMemsetAsync(h->rcount.p, 0, sizeof(unsigned long long), st));
+      if ((rc = run_fused(h, pl, nq, h->ntotal, 1, ip, st))) return rc;
+      CK(cudaMemcpyAsync(&n, h->rcount.p, sizeof(n), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (n <= h->r_cap) break;
+      want = n;  // every candidate was counted: one rerun with room for all of them
+    }
+    if (n > 0xFFFFFFFFull) return set_err(FK_E_UNSUPPORTED, "range search with %llu candidates", n);
+    // exact direct distances + radius test + sort keys
+    if ((rc = h->rdist.ensure(n * sizeof(float) + 16))) return rc;
+    if ((rc = h->rkid.ensure(n * 8 + 16)) || (rc = h->rkrd.ensure(n * 8 + 16))) return rc;
+    if ((rc = h->rkeep.ensure(n * 4 + 16)) || (rc = h->rrowc.ensure((size_t)nq * 4))) return rc;
+    CK(cudaMemsetAsync(h->rrowc.p, 0, (size_t)nq * 4, st));
+    auto rd = static_cast<float*>(h->rdist.p);
+    auto kid = static_cast<unsigned long long*>(h->rkid.p);
+    auto krd = static_cast<unsigned long long*>(h->rkrd.p);
+    auto keep = static_cast<unsigned int*>(h->rkeep.p);
+    auto rowc = static_cast<unsigned int*>(h->rrowc.p);
+    const auto cand = static_cast<const unsigned long long*>(h->rcand.p);
+    if (n > 0) {
+      const unsigned grid = (unsigned)((n + 7) / 8);
+      if (h->storage == FK_F32)
+        range_exact_kernel<0><<<grid, 256, 0, st>>>(cand, n, h->q0.p, h->q1.p, h->s0, h->s1, h->d, h->dp, ip, 0, radius,
+                                                    h->ids, rd, kid, krd, keep, rowc);
+      else if (h->storage == FK_F16)
+        range_exact_kernel<1><<<grid, 256, 0, st>>>(cand, n, h->q0.p, nullptr, h->s0, nullptr, h->d, h->dp, ip, 0,
+                                                    radius, h->ids, rd, kid, krd, keep, rowc);
+      else
+        range_exact_kernel<2><<<grid, 256, 0, st>>>(cand, n, h->q0.p, nullptr, h->s0, nullptr, h->d, h->dp, ip,
+                                                    h->fold, radius, h->ids, rd, kid, krd, keep, rowc);
+      CKL();
+    }
+    // survivors -> (row, value, id) order: stable LSD radix passes (id, then row|value)
+    if ((rc = h->rv1.ensure(n * 4 + 16)) || (rc = h->rv2.ensure(n * 4 + 16)) || (rc = h->rsel.ensure(n * 4 + 16)) ||
+        (rc = h->rnsel.ensure(16)) || (rc = h->rkid2.ensure(n * 8 + 16)) || (rc = h->rkrd2.ensure(n * 8 + 16)))
+      return rc;
+    auto v1 = static_cast<unsigned int*>(h->rv1.p);
+    auto v2 = static_cast<unsigned int*>(h->rv2.p);
+    auto sel = static_cast<unsigned int*>(h->rsel.p);
+    auto kid2 = static_cast<unsigned long long*>(h->rkid2.p);
+    auto krd2 = static_cast<unsigned long long*>(h->rkrd2.p);
+    int64_t nsel = 0;
+    if (n > 0) {
+      iota_u32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(v1, (int64_t)n);
+      size_t tb = 0;
+      CK(cub::DeviceSelect::Flagged(nullptr, tb, v1, keep, sel, static_cast<int64_t*>(h->rnsel.p), (int64_t)n, st));
+      if ((rc = h->rtmp.ensure(tb))) return rc;
+      CK(cub::DeviceSelect::Flagged(h->rtmp.p, tb, v1, keep, sel, static_cast<int64_t*>(h->rnsel.p), (int64_t)n, st));
+      CK(cudaMemcpyAsync(&nsel, h->rnsel.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    }
+    if (nsel > 0) {
+      const unsigned g = (unsigned)((nsel + 255) / 256);
+      int row_bits = 1;
+      while ((1ll << row_bits) < nq) ++row_bits;
+      gather_u64_kernel<<<g, 256, 0, st>>>(sel, kid, nsel, kid2);  // ids of the survivors
+      CKL();
+      size_t tb1 = 0, tb2 = 0;
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, tb1, kid2, krd2, sel, v1, nsel, 0, 64, st));
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, tb2, kid2, krd2, v1, v2, nsel, 0, 32 + row_bits, st));
+      if ((rc = h->rtmp.ensure(std::max(tb1, tb2)))) return rc;
+      // pass 1: by user id (flat.py:137, the secondary key)
+      CK(cub::DeviceRadixSort::SortPairs(h->rtmp.p, tb1, kid2, krd2, sel, v1, nsel, 0, 64, st));
+      // pass 2 (stable): by (row, best-first value)
+      gather_u64_kernel<<<g, 256, 0, st>>>(v1, krd, nsel, kid2);
+      CKL();
+      CK(cub::DeviceRadixSort::SortPairs(h->rtmp.p, tb2, kid2, krd2, v1, v2, nsel, 0, 32 + row_bits, st));
+      if ((rc = h->rids.ensure(nsel * 8)) || (rc = h->rdist_out.ensure(nsel * 4))) return rc;
+      gather_range_kernel<<<g, 256, 0, st>>>(v2, kid, rd, nsel, static_cast<int64_t*>(h->rids.p),
+                                             static_cast<float*>(h->rdist_out.p));
+      CKL();
+    }
+    h->r_total = nsel;
+    // lims = exclusive scan of the per-row survivor counts (nq + 1 entries)
+    if ((rc = h->rv1.ensure((size_t)(nq + 1) * 8))) return rc;
+    auto cnt64 = static_cast<int64_t*>(h->rv1.p);
+    counts_to_i64_kernel<<<(unsigned)((nq + 256) / 256), 256, 0, st>>>(rowc, nq, cnt64);
+    CKL();
+    size_t tbs = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tbs, cnt64, dlims, nq + 1, st));
+    if ((rc = h->rtmp.ensure(tbs))) return rc;
+    CK(cub::DeviceScan::ExclusiveSum(h->rtmp.p, tbs, cnt64, dlims, nq + 1, st));
+  }
+  CK(cudaMemcpyAsync(lims, dlims, (size_t)(nq + 1) * sizeof(int64_t),
+                     on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  *total = h->r_total;
+  return FK_OK;
+}
+
+int fk_range_fetch(fk_index* h, int64_t* ids, float* dist, int on_device, void* stream) {
+  if (!h) return set_err(FK_E_INVALID, "NULL index");
+  std::lock_guard<std::mutex> g(h->mu);
+  if (h->r_total == 0) return FK_OK;
+  if (!ids || !dist) return set_err(FK_E_INVALID, "NULL output pointer");
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  CK(cudaMemcpyAsync(ids, h->rids.p, (size_t)h->r_total * sizeof(int64_t), kind, st));
+  CK(cudaMemcpyAsync(dist, h->rdist_out.p, (size_t)h->r_total * sizeof(float), kind, st));
+  CK(cudaStreamSynchronize(st));
+  return FK_OK;
+}
 
 int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D, int64_t* I, int64_t* P,
               int on_device, void* stream) {

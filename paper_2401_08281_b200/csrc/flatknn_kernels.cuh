@@ -72,6 +72,13 @@ struct SearchParams {
   int cluster;     // 1, or 2: CTA pairs share each base tile (each loads half, TMA multicast to both)
   int num_mu;      // query-tile units per chunk: num_m, or ceil(num_m / 2) pairs in cluster mode
   int bn;          // base rows per tile (template TBN of the launched kernel)
+  // range search (KQ == -1): every (row, position) whose fast-filter value
+  // passes the conservative radius bound is appended to rcand (the exact
+  // direct distance and the radius test follow in range_exact_kernel)
+  float radius;
+  unsigned long long* rcand;  // [rcap] (row << 32 | position)
+  unsigned long long* rcount; // device counter (may exceed rcap: caller grows and reruns)
+  unsigned long long rcap;
   int dbg_flags;   // bottleneck experiments: 1 = epilogue skips compute, 2 = producer skips TMA
 };
 
@@ -571,7 +578,8 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         if (lane == 0) mbar_arrive(afull);
       }
 
-      const float qn = (!IS_IP && row_ok) ? p.qnorm[row] : 0.f;
+      constexpr bool RANGE = KQ < 0;
+      const float qn = ((!IS_IP || RANGE) && row_ok) ? p.qnorm[row] : 0.f;
       constexpr int KQS = KQ > 0 ? KQ : 1;
       uint32_t keys[KQS], pos[KQS];
       if constexpr (KQ > 0) {
@@ -593,14 +601,20 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       };
       // Effective threshold = min(own k-th, best k-th published by any unit of
       // this query): every true top-k member has key <= the global k-th <= it.
-      uint32_t gkey = row_ok ? __ldcg(p.thr_key + row) : 0xFFFFFFFFu;
+      uint32_t gkey = (row_ok && !RANGE) ? __ldcg(p.thr_key + row) : 0xFFFFFFFFu;
       float thr = unmonotone(gkey);  // NaN while nothing is known: everything passes
+      if constexpr (RANGE) thr = IS_IP ? -p.radius : p.radius;  // IP ranks -ip (core.py:217)
       // Conservative fast-filter bound on f = fl(xn - 2ip): the reference value
       // fl(fl(qn + xn) - 2ip) differs from qn + f by < 3u(qn + xn + |v|); the
       // 2^-20 margin (u = 2^-24) over max-norm covers it with room to spare.
       const float xmax = IS_IP ? 0.f : *p.xn_max;
       auto filter_bound = [&](float th) -> float {
-        if (IS_IP) return th;
+        if (IS_IP) {
+          // range search compares the GEMM inner product with the exact
+          // direct one: widen by 2^-18 |q| max|x| (>> the 3xTF32 / fp32 error)
+          if (RANGE) return th + 3.814697265625e-06f * sqrtf(qn * *p.xn_max);
+          return th;
+        }
         return (th - qn) + (qn + xmax + fabsf(th)) * 9.5367431640625e-07f;
       };
       float T = filter_bound(thr);
@@ -683,6 +697,20 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) cand |= ((IS_IP ? !(-f[j] > T) : !(f[j] > T)) ? 1u : 0u) << j;
           cand &= valid;
+          if constexpr (RANGE) {  // append every candidate; the exact test happens later
+            const unsigned nc = __popc(cand);
+            if (nc) {
+              unsigned long long slot = atomicAdd(p.rcount, (unsigned long long)nc);
+              while (cand) {
+                const int j = __ffs(cand) - 1;
+                cand &= cand - 1;
+                if (slot < p.rcap)
+                  p.rcand[slot] = (static_cast<unsigned long long>(row) << 32) | static_cast<uint32_t>(n0 + c0 + j);
+                ++slot;
+              }
+            }
+            return;
+          }
           while (cand) {
             const int j = __ffs(cand) - 1;
             cand &= cand - 1;
@@ -759,7 +787,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         __syncwarp();
         if (tr) p.trace[tcount * 16 + 7] = clock64();
         if (lane == 0 && XN_TILE) mbar_arrive(&xempty[xslot]);
-        if ((++own_tiles & 15) == 0 && row_ok) {  // publish own k-th, fetch the shared bound
+        if (!RANGE && (++own_tiles & 15) == 0 && row_ok) {  // publish own k-th, fetch the shared bound
           const uint32_t mine = own_key();
           gkey = min(atomicMin(p.thr_key + row, mine), mine);
           thr = unmonotone(min(mine, gkey));
@@ -768,7 +796,9 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       }
       const int S_tot = p.S * NH;
       const size_t base = ((size_t)row * S_tot + chunk * NH + h) * (size_t)k;
-      if constexpr (KQ > 0) {
+      if constexpr (RANGE) {
+        // nothing per unit: candidates went straight to rcand
+      } else if constexpr (KQ > 0) {
         if (row_ok) {
           atomicMin(p.thr_key + row, keys[KQ - 1]);
 #pragma unroll
@@ -1201,6 +1231,54 @@ __global__ void fill_sentinel_kernel(float* D, int64_t* I, int64_t* P, size_t n,
     D[i] = v;
     I[i] = -1;
     if (P) P[i] = -1;
+  }
+}
+
+// ------------------------------------------------------------ range search
+// Exact direct distance of every candidate (reference range search goes
+// through pairwise_distances -> the direct per-pair loops, flat.py:121-144,
+// _ckernels.pyx dist_one): L2 sum (q - x)^2, IP sum q x, accumulated in fp64
+// and rounded once to fp32, from the STORED operands (fp32: hi + lo == x
+// exactly; fold: -2x scaled back).  Survivors (<= radius, >= for IP) get
+// sort keys: key_id = user id, key_rd = (row << 32) | monotone(best-first value).
+template <int MODE>
+__global__ void range_exact_kernel(const unsigned long long* __restrict__ cand, unsigned long long n,
+                                   const void* __restrict__ q0, const void* __restrict__ q1, const void* __restrict__ s0,
+                                   const void* __restrict__ s1, int d, int dp, int is_ip, int fold, float radius,
+                                   const int64_t* __restrict__ ids, float* __restrict__ dist,
+                                   unsigned long long* __restrict__ key_id, unsigned long long* __restrict__ key_rd,
+                                   unsigned int* __restrict__ keep, unsigned int* __restrict__ row_count) {
+  const unsigned long long i = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const unsigned long long e = cand[i];
+  const uint32_t row = static_cast<uint32_t>(e >> 32), pos = static_cast<uint32_t>(e);
+  auto val = [&](const void* a, const void* b, size_t off) -> double {
+    if (MODE == 0) return (double)(static_cast<const float*>(a)[off] + static_cast<const float*>(b)[off]);
+    if (MODE == 1) return (double)__half2float(static_cast<const __half*>(a)[off]);
+    return (double)__bfloat162float(static_cast<const __nv_bfloat16*>(a)[off]);
+  };
+  double acc = 0.0;
+  for (int c = lane; c < d; c += 32) {
+    const double qv = val(q0, q1, (size_t)row * dp + c);
+    double xv = val(s0, s1, (size_t)pos * dp + c);
+    if (fold) xv *= -0.5;  // stored -2x (exact)
+    if (is_ip) acc = fma(qv, xv, acc);
+    else {
+      const double t = qv - xv;
+      acc = fma(t, t, acc);
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(FULLMASK, acc, off);
+  if (lane == 0) {
+    const float v = static_cast<float>(acc);
+    const bool in = is_ip ? (v >= radius) : (v <= radius);  // flat.py:134 (NaN never matches)
+    keep[i] = in ? 1u : 0u;
+    dist[i] = v;
+    key_id[i] = static_cast<unsigned long long>(ids[pos]);
+    key_rd[i] = (static_cast<unsigned long long>(row) << 32) | monotone(is_ip ? -v : v);
+    if (in) atomicAdd(row_count + row, 1u);
   }
 }
 

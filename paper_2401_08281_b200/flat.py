@@ -21,7 +21,8 @@ import ctypes
 import numpy as np
 
 from . import _native as N
-from .core import METRIC_IP, METRIC_L2, Index, Metric, SearchResult, as_vectors, is_torch, metric_value
+from .core import (METRIC_IP, METRIC_L2, Index, Metric, RangeResult, SearchResult, as_vectors, is_torch,
+                   metric_value)
 
 try:
     import torch
@@ -181,6 +182,32 @@ class FlatIndex(Index):
                                 P.ctypes.data if P is not None else None, 0, 0))
         res = SearchResult(I, D, k)
         return (res, P) if with_positions else res
+
+    def _range_search(self, q, radius: float) -> RangeResult:
+        """flat.py:121-144 on the GPU: direct distances (<= radius; >= for
+        IP), each query's list best first, ties by smaller id (flat.py:137)."""
+        nq = q.shape[0]
+        L = N.lib()
+        total = ctypes.c_int64(0)
+        if is_torch(q) and q.is_cuda:
+            if q.device.index != self.device:
+                q = q.to(f"cuda:{self.device}")
+            lims = torch.empty(nq + 1, dtype=torch.int64, device=q.device)
+            N.check(L.fk_range_search(self._h, _ptr(q), nq, _dtype_code(q), float(radius), _ptr(lims),
+                                      ctypes.byref(total), 1, _stream_of(self.device)))
+            ids = torch.empty(total.value, dtype=torch.int64, device=q.device)
+            dist = torch.empty(total.value, dtype=torch.float32, device=q.device)
+            N.check(L.fk_range_fetch(self._h, _ptr(ids), _ptr(dist), 1, _stream_of(self.device)))
+        else:
+            if is_torch(q):
+                q = q.contiguous()
+            lims = np.empty(nq + 1, dtype=np.int64)
+            N.check(L.fk_range_search(self._h, _ptr(q), nq, _dtype_code(q), float(radius), lims.ctypes.data,
+                                      ctypes.byref(total), 0, 0))
+            ids = np.empty(total.value, dtype=np.int64)
+            dist = np.empty(total.value, dtype=np.float32)
+            N.check(L.fk_range_fetch(self._h, ids.ctypes.data, dist.ctypes.data, 0, 0))
+        return RangeResult(lims, ids, dist, float(radius))
 
     def search_with_positions(self, q, k: int):
         """Search returning (SearchResult, storage positions) -- the sharded

@@ -73,3 +73,35 @@ def assert_parity(got_ids, got_dist, ref_ids, ref_dist, **kw):
     assert s["set_bad"] == 0, s
     assert s["tie_recall"] == 1.0, s
     return s
+
+
+def assert_range_parity(got, want, radius, metric, rel_tie=1e-5, abs_tie=1e-6, rel_dist=1e-4, abs_dist=1e-5,
+                        exact=False):
+    """Range-search parity (flat.py:121-144 semantics): per query the id sets
+    agree except ids whose distance is within ``rel_tie`` of the radius
+    (boundary near-ties), common ids agree on distance, and the returned list
+    is best first with ties by smaller id.  ``exact``: identical CSR output
+    (integer-valued data, where every distance is exact)."""
+    (gl, gi, gd), (wl, wi, wd) = [tuple(np.asarray(a.cpu() if hasattr(a, "cpu") else a) for a in t) for t in (got, want)]
+    assert gl.shape == wl.shape, (gl.shape, wl.shape)
+    if exact:
+        assert np.array_equal(gl, wl) and np.array_equal(gi, wi)
+        assert np.array_equal(gd.astype(np.float32), wd.astype(np.float32))
+        return
+    desc = metric == "ip"
+    rad = float(radius)
+    for r in range(len(gl) - 1):
+        g_ids, g_d = gi[gl[r]:gl[r + 1]], gd[gl[r]:gl[r + 1]].astype(np.float64)
+        w_ids, w_d = wi[wl[r]:wl[r + 1]], wd[wl[r]:wl[r + 1]].astype(np.float64)
+        gm, wm = dict(zip(g_ids.tolist(), g_d)), dict(zip(w_ids.tolist(), w_d))
+        near = lambda v: np.isfinite(rad) and abs(v - rad) <= rel_tie * max(abs(rad), abs(v)) + abs_tie  # noqa: E731
+        for i in set(wm) - set(gm):
+            assert near(wm[i]), f"row {r}: id {i} (d={wm[i]!r}) missing, radius {rad!r}"
+        for i in set(gm) - set(wm):
+            assert near(gm[i]), f"row {r}: extra id {i} (d={gm[i]!r}), radius {rad!r}"
+        for i in set(gm) & set(wm):
+            assert abs(gm[i] - wm[i]) <= rel_dist * abs(wm[i]) + abs_dist, (r, i, gm[i], wm[i])
+        # best first, ties by smaller id, on our own values
+        key = -g_d if desc else g_d
+        for a in range(len(g_ids) - 1):
+            assert key[a] < key[a + 1] or (key[a] == key[a + 1] and g_ids[a] < g_ids[a + 1]), (r, a)
