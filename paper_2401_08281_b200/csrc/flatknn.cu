@@ -621,6 +621,8 @@ int run_fused(fk_index* h, const Plan& P, int64_t nq, int64_t nb_pass, int k, bo
     sp.kk_last = (last + kstep - 1) / kstep;
   }
   sp.n_issuers = P.n_issuers;
+  sp.n_producers = P.n_issuers == 2 ? 2 : 1;
+  if (const char* e = getenv("FK_PRODUCERS")) sp.n_producers = (atoi(e) == 1 || P.n_issuers == 1) ? 1 : 2;
   sp.cluster = P.cluster;
   sp.bn = P.bn;
   sp.radius = h->r_radius;

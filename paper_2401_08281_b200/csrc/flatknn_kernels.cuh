@@ -66,6 +66,7 @@ struct SearchParams {
   int xn_slots;    // base-norm tile ring depth (prefetched by the producer)
   unsigned long long* trace;  // debug timeline (CTA 0): [tile][16] clock64 stamps
   int n_issuers;   // MMA-issuing threads (warps 1 and 3)
+  int n_producers; // TMA producer threads: 1 (warp 0 serves every ring) or one per issuer ring (warps 0, 2)
   int acc_stages;  // TMEM accumulator buffers (2..4); the query operand (a_mode 0) follows them
   int kk_last;     // MMA K-steps in the last 128-byte K-chunk (trims the zero padding of d)
   int b_policy;    // L2 eviction policy of the streamed base tiles (0 first, 1 normal, 2 last)
@@ -345,7 +346,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0 || (warp == 2 && p.n_issuers == 2)) {
+  if (warp == 0 || (warp == 2 && p.n_issuers == 2 && p.n_producers == 2)) {
     // ===================== TMA producers =====================
     // One producer per MMA issuer (warp 0 -> ring 0, warp 2 -> ring 1): a
     // producer blocked on one ring's free slots never stalls the other ring.
@@ -358,9 +359,11 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       // one FIFO sub-ring of `sh` slots per MMA issuer (tile t -> ring t % nis)
       const uint32_t nis = p.n_issuers;
       const uint32_t sh = (uint32_t)stages / nis;
-      uint32_t rs = 0, rph = 0;  // position in my sub-ring
-      const uint32_t xh = (uint32_t)xn_slots / nis;  // my norm-tile sub-ring: slots [myring*xh, +xh)
-      uint32_t xt = 0, xphase = 0, tc = 0;
+      // per-ring positions (a single producer serves both rings when
+      // n_producers == 1); norm-tile sub-ring of ring r: slots [r*xh, +xh)
+      uint32_t rs0 = 0, rph0 = 0, rs1 = 0, rph1 = 0, xt0 = 0, xp0 = 0, xt1 = 0, xp1 = 0;
+      const uint32_t xh = (uint32_t)xn_slots / nis;
+      uint32_t tc = 0;
       int j = 0;
       for (int u = ublock; u < p.num_units; u += ugrid, ++j) {
         const int chunk = u / p.num_mu;
@@ -377,9 +380,13 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         }
         for (int t = t0; t < t1; ++t, ++tc) {
           const uint32_t ring = (nis == 2) ? (tc & 1) : 0;
-          if (ring != myring) continue;  // the other producer's tile
-          if (XN_TILE) {  // base norms of this tile -> my norm sub-ring (consumed by the epilogue)
-            const uint32_t xs = myring * xh + xt, xph = xphase;
+          if (p.n_producers == 2 && ring != myring) continue;  // the other producer's tile
+          uint32_t& rs = ring ? rs1 : rs0;
+          uint32_t& rph = ring ? rph1 : rph0;
+          if (XN_TILE) {  // base norms of this tile -> the ring's norm sub-ring (consumed by the epilogue)
+            uint32_t& xt = ring ? xt1 : xt0;
+            uint32_t& xphase = ring ? xp1 : xp0;
+            const uint32_t xs = ring * xh + xt, xph = xphase;
             if (++xt == xh) {
               xt = 0;
               xphase ^= 1;
