@@ -130,6 +130,7 @@ struct DevBuf {
 struct fk_index {
   int device = 0, d = 0, dp = 0, metric = FK_METRIC_L2, storage = FK_F32;
   int fold = 0;  // bf16 L2 with d+3 <= dp: norms folded into the GEMM operands (MODE 3 kernels)
+  int split = 1;  // fp32: 2 = 3xTF32 hi/lo split (MODE 0), 1 = raw fp32 + TF32 filter + exact rescoring (MODE 4)
   int64_t ntotal = 0, cap = 0;
   void* s0 = nullptr;        // stored operand (hi / f16 / bf16) [cap][dp]
   void* s1 = nullptr;        // lo part (fp32 mode) [cap][dp]
@@ -182,7 +183,7 @@ int grow(fk_index* h, int64_t need, cudaStream_t st) {
   float* nn = nullptr;
   int64_t* ni = nullptr;
   cudaError_t e = cudaMalloc(&n0, nc * rb);
-  if (e == cudaSuccess && h->storage == FK_F32) e = cudaMalloc(&n1, nc * rb);
+  if (e == cudaSuccess && h->split == 2) e = cudaMalloc(&n1, nc * rb);
   if (e == cudaSuccess) e = cudaMalloc((void**)&nn, nc * sizeof(float));
   if (e == cudaSuccess) e = cudaMalloc((void**)&ni, nc * sizeof(int64_t));
   if (e != cudaSuccess) {
@@ -212,14 +213,23 @@ int grow(fk_index* h, int64_t need, cudaStream_t st) {
   return FK_OK;
 }
 
-int launch_prep(int storage, const void* x, int dtype, int64_t n, int d, int dp, void* o0, void* o1, float* norms,
+// kernel operand mode of an index: 0 fp32 hi/lo (3xTF32), 4 fp32 raw (TF32
+// filter + exact rescoring), 1 fp16, 2 bf16 (3 = bf16 with folded norms)
+int kmode_of(const fk_index* h) {
+  if (h->storage == FK_F32) return h->split == 2 ? 0 : 4;
+  return h->storage == FK_F16 ? 1 : 2;
+}
+
+int launch_prep(int kmode, const void* x, int dtype, int64_t n, int d, int dp, void* o0, void* o1, float* norms,
                 int64_t row0, cudaStream_t st, int fold = 0) {
   if (n <= 0) return FK_OK;
   const int wpb = 8;
   const unsigned grid = (unsigned)((n + wpb - 1) / wpb);
-  if (storage == FK_F32)
+  if (kmode == 0)
     prep_rows_kernel<0><<<grid, wpb * 32, 0, st>>>(x, dtype, n, d, dp, o0, o1, norms, row0, 0);
-  else if (storage == FK_F16)
+  else if (kmode == 4)
+    prep_rows_kernel<4><<<grid, wpb * 32, 0, st>>>(x, dtype, n, d, dp, o0, o1, norms, row0, 0);
+  else if (kmode == 1)
     prep_rows_kernel<1><<<grid, wpb * 32, 0, st>>>(x, dtype, n, d, dp, o0, o1, norms, row0, 0);
   else
     prep_rows_kernel<2><<<grid, wpb * 32, 0, st>>>(x, dtype, n, d, dp, o0, o1, norms, row0, fold);
@@ -265,7 +275,7 @@ template <int MODE, int KQ, bool IP, int EPI>
 int launch_fused_t(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0, const CUtensorMap& b1,
                    const SearchParams& sp, int grid, int smem, cudaStream_t st) {
   if (sp.bn == 64) {
-    if constexpr ((MODE == 0) == (EPI == 4))
+    if constexpr ((MODE == 0 || MODE == 4) == (EPI == 4))
       return launch_fused_tb<MODE, KQ, IP, EPI, 64>(a0, a1, b0, b1, sp, grid, smem, st);
     return set_err(FK_E_UNSUPPORTED, "64-column tiles need the default epilogue width");
   }
@@ -281,20 +291,24 @@ int launch_fused_k(int kq, const CUtensorMap& a0, const CUtensorMap& a1, const C
     case 32: return launch_fused_t<MODE, 32, IP, EPI>(a0, a1, b0, b1, sp, grid, smem, st);
     case 0: return launch_fused_t<MODE, 0, IP, EPI>(a0, a1, b0, b1, sp, grid, smem, st);
     case -1:  // range search: default epilogue width only
-      if constexpr ((MODE == 0) == (EPI == 4)) return launch_fused_t<MODE, -1, IP, EPI>(a0, a1, b0, b1, sp, grid, smem, st);
+      if constexpr ((MODE == 0 || MODE == 4) == (EPI == 4))
+        return launch_fused_t<MODE, -1, IP, EPI>(a0, a1, b0, b1, sp, grid, smem, st);
       return set_err(FK_E_UNSUPPORTED, "range search runs with the default epilogue width");
   }
   return set_err(FK_E_UNSUPPORTED, "queue bucket %d", kq);
 }
 
 template <int EPI>
-int launch_fused_e(int storage, bool fold, bool ip, int kq, const CUtensorMap& a0, const CUtensorMap& a1,
+int launch_fused_e(int kmode, bool fold, bool ip, int kq, const CUtensorMap& a0, const CUtensorMap& a1,
                    const CUtensorMap& b0, const CUtensorMap& b1, const SearchParams& sp, int grid, int smem,
                    cudaStream_t st) {
-  if (storage == FK_F32)
+  if (kmode == 0)
     return ip ? launch_fused_k<0, true, EPI>(kq, a0, a1, b0, b1, sp, grid, smem, st)
               : launch_fused_k<0, false, EPI>(kq, a0, a1, b0, b1, sp, grid, smem, st);
-  if (storage == FK_F16)
+  if (kmode == 4)
+    return ip ? launch_fused_k<4, true, EPI>(kq, a0, a1, b0, b1, sp, grid, smem, st)
+              : launch_fused_k<4, false, EPI>(kq, a0, a1, b0, b1, sp, grid, smem, st);
+  if (kmode == 1)
     return ip ? launch_fused_k<1, true, EPI>(kq, a0, a1, b0, b1, sp, grid, smem, st)
               : launch_fused_k<1, false, EPI>(kq, a0, a1, b0, b1, sp, grid, smem, st);
   if (fold && !ip) return launch_fused_k<3, false, EPI>(kq, a0, a1, b0, b1, sp, grid, smem, st);
@@ -302,11 +316,11 @@ int launch_fused_e(int storage, bool fold, bool ip, int kq, const CUtensorMap& a
             : launch_fused_k<2, false, EPI>(kq, a0, a1, b0, b1, sp, grid, smem, st);
 }
 
-int launch_fused(int epi, int storage, bool fold, bool ip, int kq, const CUtensorMap& a0, const CUtensorMap& a1,
+int launch_fused(int epi, int kmode, bool fold, bool ip, int kq, const CUtensorMap& a0, const CUtensorMap& a1,
                  const CUtensorMap& b0, const CUtensorMap& b1, const SearchParams& sp, int grid, int smem,
                  cudaStream_t st) {
-  if (epi == 8) return launch_fused_e<8>(storage, fold, ip, kq, a0, a1, b0, b1, sp, grid, smem, st);
-  return launch_fused_e<4>(storage, fold, ip, kq, a0, a1, b0, b1, sp, grid, smem, st);
+  if (epi == 8) return launch_fused_e<8>(kmode, fold, ip, kq, a0, a1, b0, b1, sp, grid, smem, st);
+  return launch_fused_e<4>(kmode, fold, ip, kq, a0, a1, b0, b1, sp, grid, smem, st);
 }
 
 // Split-N plan: choose the number of N-chunks S so that num_m*S work units
@@ -374,6 +388,13 @@ int fk_create(int device, int d, int metric, int storage, fk_index** out) {
   // bf16 L2 with >= 3 free padding columns: fold the norms into the operands
   // (FK_NO_FOLD=1 keeps the separate norm tile; tests compare both layouts)
   h->fold = storage == FK_BF16 && metric == FK_METRIC_L2 && d + 3 <= h->dp;
+  // fp32: raw storage + 1-pass TF32 filter with exact fp32 rescoring of the
+  // survivors (FK_FP32_ALGO=1, experimental) or the 3xTF32 hi/lo split (default)
+  h->split = 1;
+  if (storage == FK_F32) {
+    h->split = 2;
+    if (const char* e = getenv("FK_FP32_ALGO"); e && atoi(e) == 1) h->split = 1;
+  }
   if (const char* e = getenv("FK_NO_FOLD"); e && atoi(e)) h->fold = 0;
   h->num_sms = prop.multiProcessorCount;
   if (cudaMalloc((void**)&h->xn_max, sizeof(float)) != cudaSuccess || cudaMemset(h->xn_max, 0, sizeof(float)) != cudaSuccess) {
@@ -439,7 +460,7 @@ int fk_add(fk_index* h, const void* x, int64_t n, int dtype, const int64_t* ids,
       CK(cudaMemcpyAsync(h->stage_in.p, src, m * in_row, cudaMemcpyHostToDevice, st));
       src = h->stage_in.p;
     }
-    if ((rc = launch_prep(h->storage, src, dtype, m, h->d, h->dp, h->s0, h->s1, h->norms, h->ntotal + r0, st,
+    if ((rc = launch_prep(kmode_of(h), src, dtype, m, h->d, h->dp, h->s0, h->s1, h->norms, h->ntotal + r0, st,
                           h->fold ? 1 : 0)))
       return rc;
     if (!on_device) CK(cudaStreamSynchronize(st));  // stage buffer reused by the next slice
@@ -478,10 +499,10 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   if (const char* e = getenv("FK_EPI"); e && kq >= 0) P.epi = atoi(e) == 8 ? 8 : 4;
   P.nh = P.epi / 4;
   P.num_m = (int)((nq + BM - 1) / BM);
-  const int split = split_of(h->storage);
+  const int split = h->split;
   const int num_kb = h->dp / chunk_elems_of(h->storage);
   const int a_bytes = split * num_kb * (int)CHUNK_BYTES;
-  const int a_tmem_cols = h->storage == FK_F32 ? 2 * h->dp : h->dp / 2;
+  const int a_tmem_cols = h->storage == FK_F32 ? split * h->dp : h->dp / 2;
   // Query operand placement and tile width:
   //  * 16-bit with two epilogue groups: the accumulator ring wants 4 buffers
   //    (an even count, see below), so A goes to smem (SS MMA) when it fits;
@@ -498,7 +519,10 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   } else P.a_mode = 1;
   if (const char* e = getenv("FK_FORCE_AMODE")) P.a_mode = std::max(0, std::min(2, atoi(e)));
   if (const char* e = getenv("FK_BN")) P.bn = atoi(e) == 64 ? 64 : 128;
-  if (P.a_mode == 0 && a_tmem_cols > 512 - 2 * P.bn) P.a_mode = 1;
+  // single accumulator (FK_ACC=1): A may take up to 512 - TBN columns; the
+  // MMA then waits for each tile's readout (one issuer, one epilogue group)
+  const bool single_acc = getenv("FK_ACC") && atoi(getenv("FK_ACC")) == 1;
+  if (P.a_mode == 0 && a_tmem_cols > 512 - (single_acc ? 1 : 2) * P.bn) P.a_mode = 1;
   if (P.a_mode != 0) P.bn = 128;
   if (P.bn == 64) {  // 64-column kernels exist only for the default epilogue width
     P.epi = h->storage == FK_F32 ? 4 : 8;
@@ -514,9 +538,11 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   if (P.num_m < 2 || h->num_sms < 2) P.cluster = 1;
   P.num_mu = (P.num_m + P.cluster - 1) / P.cluster;
   // chunk <= L2_CHUNK_BYTES of streamed base; partial lists <= PARTIAL_BYTES
-  const size_t tile_bytes = (size_t)bn * h->dp * elem_bytes_of(h->storage) * split_of(h->storage);
+  const size_t tile_bytes = (size_t)bn * h->dp * elem_bytes_of(h->storage) * h->split;
   // (very large k: partial lists are k deep, so merge cost grows with S -> 4x window)
-  const int max_chunk = std::max<int>(64, (int)(L2_CHUNK_BYTES * (k >= 512 ? 4 : 1) / tile_bytes));
+  size_t l2_chunk = L2_CHUNK_BYTES;
+  if (const char* e = getenv("FK_L2_CHUNK_MB")) l2_chunk = (size_t)std::max(1, atoi(e)) << 20;
+  const int max_chunk = std::max<int>(16, (int)(l2_chunk * (k >= 512 ? 4 : 1) / tile_bytes));
   const int min_S = (P.n_tiles + max_chunk - 1) / max_chunk;
   const size_t list_bytes = (size_t)nq * P.nh * std::max(k, 1) * 8;  // one chunk's partial lists
   const int max_S = (int)std::max<size_t>(1, std::min<size_t>(PARTIAL_BYTES / list_bytes, 1 << 20));
@@ -550,13 +576,18 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   if (P.stages < 2) return set_err(FK_E_UNSUPPORTED, "pipeline does not fit in shared memory");
   // TMEM: 512 columns = acc_stages x 128-column accumulators (+ the query operand in a_mode 0)
   P.acc_stages = std::min(4, (512 - (P.a_mode == 0 ? a_tmem_cols : 0)) / bn);
-  if (const char* e = getenv("FK_ACC")) P.acc_stages = std::max(2, std::min(P.acc_stages, atoi(e)));
+  if (const char* e = getenv("FK_ACC")) P.acc_stages = std::max(1, std::min(P.acc_stages, atoi(e)));
   P.n_issuers = P.stages >= 4 ? 2 : 1;  // each issuer needs a sub-ring of >= 2 slots
   if (const char* e = getenv("FK_ISSUERS")) P.n_issuers = (atoi(e) == 1 || P.stages < 4) ? 1 : 2;
   // Tiles alternate between the 2 MMA issuers and between the NH epilogue
   // groups; each party must wait on EVERY phase of the buffers it uses (an
   // mbarrier parity wait cannot skip a phase), so buffer = tile % acc_stages
   // must map each party onto its own buffers: acc_stages % parties == 0.
+  if (P.acc_stages == 1) {  // one buffer: one issuer and one epilogue group wait on every phase
+    P.n_issuers = 1;
+    P.epi = 4;
+    P.nh = 1;
+  }
   if ((P.n_issuers == 2 || P.nh == 2) && (P.acc_stages & 1)) P.acc_stages -= 1;
   P.smem = SMEM_RESERVE + hist_bytes + xn_bytes + (P.a_mode == 1 ? a_bytes : 0) + P.stages * stage_bytes_for(P.a_mode);
   P.S_tot = P.S * P.nh;
@@ -580,7 +611,7 @@ int run_fused(fk_index* h, const Plan& P, int64_t nq, int64_t nb_pass, int k, bo
   if ((rc = make_map(&ta0, h->q0.p, eb, h->dp, nq))) return rc;
   const uint32_t b_rows = P.cluster == 2 ? P.bn / 2 : P.bn;  // cluster mode: each CTA loads half a tile
   if ((rc = make_map(&tb0, h->s0, eb, h->dp, nb_pass, b_rows))) return rc;
-  if (h->storage == FK_F32) {
+  if (h->split == 2) {
     if ((rc = make_map(&ta1, h->q1.p, eb, h->dp, nq))) return rc;
     if ((rc = make_map(&tb1, h->s1, eb, h->dp, nb_pass, b_rows))) return rc;
   } else {
@@ -625,6 +656,7 @@ int run_fused(fk_index* h, const Plan& P, int64_t nq, int64_t nb_pass, int k, bo
   if (const char* e = getenv("FK_PRODUCERS")) sp.n_producers = (atoi(e) == 1 || P.n_issuers == 1) ? 1 : 2;
   sp.cluster = P.cluster;
   sp.bn = P.bn;
+  sp.xbase = h->s0;
   sp.radius = h->r_radius;
   sp.rcand = static_cast<unsigned long long*>(h->rcand.p);
   sp.rcount = static_cast<unsigned long long*>(h->rcount.p);
@@ -632,7 +664,7 @@ int run_fused(fk_index* h, const Plan& P, int64_t nq, int64_t nb_pass, int k, bo
   sp.num_mu = P.num_mu;
   if (const char* e = getenv("FK_DEBUG_FLAGS")) sp.dbg_flags = atoi(e);
   if (const char* e = getenv("FK_B_POLICY")) sp.b_policy = atoi(e);
-  rc = launch_fused(P.epi, h->storage, h->fold != 0, ip, P.kq, ta0, ta1, tb0, tb1, sp, P.grid, P.smem, st);
+  rc = launch_fused(P.epi, kmode_of(h), h->fold != 0, ip, P.kq, ta0, ta1, tb0, tb1, sp, P.grid, P.smem, st);
   if (rc == FK_OK) h->nlaunch++;
   return rc;
 }
@@ -691,9 +723,9 @@ int stage_queries(fk_index* h, const void* q, int64_t nq, int dtype, int on_devi
   }
   const size_t qrow = row_bytes(h);
   if ((rc = h->q0.ensure(nq * qrow))) return rc;
-  if (h->storage == FK_F32 && (rc = h->q1.ensure(nq * qrow))) return rc;
+  if (h->split == 2 && (rc = h->q1.ensure(nq * qrow))) return rc;
   if ((rc = h->qn.ensure(nq * sizeof(float)))) return rc;
-  return launch_prep(h->storage, qsrc, dtype, nq, h->d, h->dp, h->q0.p, h->q1.p, static_cast<float*>(h->qn.p), 0, st,
+  return launch_prep(kmode_of(h), qsrc, dtype, nq, h->d, h->dp, h->q0.p, h->q1.p, static_cast<float*>(h->qn.p), 0, st,
                      h->fold ? 2 : 0);
 }
 
@@ -777,9 +809,12 @@ int fk_range_search(fk_index* h, const void* q, int64_t nq, int dtype, float rad
     const auto cand = static_cast<const unsigned long long*>(h->rcand.p);
     if (n > 0) {
       const unsigned grid = (unsigned)((n + 7) / 8);
-      if (h->storage == FK_F32)
+      if (h->storage == FK_F32 && h->split == 2)
         range_exact_kernel<0><<<grid, 256, 0, st>>>(cand, n, h->q0.p, h->q1.p, h->s0, h->s1, h->d, h->dp, ip, 0, radius,
                                                     h->ids, rd, kid, krd, keep, rowc);
+      else if (h->storage == FK_F32)
+        range_exact_kernel<4><<<grid, 256, 0, st>>>(cand, n, h->q0.p, nullptr, h->s0, nullptr, h->d, h->dp, ip, 0,
+                                                    radius, h->ids, rd, kid, krd, keep, rowc);
       else if (h->storage == FK_F16)
         range_exact_kernel<1><<<grid, 256, 0, st>>>(cand, n, h->q0.p, nullptr, h->s0, nullptr, h->d, h->dp, ip, 0,
                                                     radius, h->ids, rd, kid, krd, keep, rowc);
@@ -903,21 +938,8 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
     const int kq = k <= 8 ? 8 : k <= 16 ? 16 : k <= 32 ? 32 : 0;  // 0: large-k buffers
 
     // ---- queries -> device operand layout + norms
-    const size_t in_row = (size_t)h->d * dtype_bytes(dtype);
-    const void* qsrc = q;
-    if (!on_device) {
-      if ((rc = h->q_in.ensure(nq * in_row))) return rc;
-      CK(cudaMemcpyAsync(h->q_in.p, q, nq * in_row, cudaMemcpyHostToDevice, st));
-      qsrc = h->q_in.p;
-    }
-    const size_t qrow = row_bytes(h);
-    if ((rc = h->q0.ensure(nq * qrow))) return rc;
-    if (h->storage == FK_F32 && (rc = h->q1.ensure(nq * qrow))) return rc;
-    if ((rc = h->qn.ensure(nq * sizeof(float)))) return rc;
     if (ev) CK(cudaEventRecord(ev[0], st));
-    if ((rc = launch_prep(h->storage, qsrc, dtype, nq, h->d, h->dp, h->q0.p, h->q1.p, static_cast<float*>(h->qn.p),
-                          0, st, h->fold ? 2 : 0)))
-      return rc;
+    if ((rc = stage_queries(h, q, nq, dtype, on_device, st))) return rc;
     h->nlaunch++;
 
     Plan pl;
@@ -1015,8 +1037,10 @@ int fk_reconstruct(fk_index* h, const int64_t* positions, int64_t n, float* out,
     dout = static_cast<float*>(h->stage_in.p);
   }
   const unsigned grid = (unsigned)((n + 7) / 8);
-  if (h->storage == FK_F32)
+  if (h->storage == FK_F32 && h->split == 2)
     reconstruct_kernel<0><<<grid, 256, 0, st>>>(h->s0, h->s1, h->dp, h->d, dpos, n, dout, 1.f);
+  else if (h->storage == FK_F32)
+    reconstruct_kernel<4><<<grid, 256, 0, st>>>(h->s0, h->s1, h->dp, h->d, dpos, n, dout, 1.f);
   else if (h->storage == FK_F16)
     reconstruct_kernel<1><<<grid, 256, 0, st>>>(h->s0, h->s1, h->dp, h->d, dpos, n, dout, 1.f);
   else

@@ -73,6 +73,7 @@ struct SearchParams {
   int cluster;     // 1, or 2: CTA pairs share each base tile (each loads half, TMA multicast to both)
   int num_mu;      // query-tile units per chunk: num_m, or ceil(num_m / 2) pairs in cluster mode
   int bn;          // base rows per tile (template TBN of the launched kernel)
+  const void* xbase;  // stored base rows (MODE 4: raw fp32, read for exact rescoring)
   // range search (KQ == -1): every (row, position) whose fast-filter value
   // passes the conservative radius bound is appended to rcand (the exact
   // direct distance and the radius test follow in range_exact_kernel)
@@ -258,9 +259,12 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     fused_knn_kernel(const __grid_constant__ CUtensorMap tm_a0, const __grid_constant__ CUtensorMap tm_a1,
                      const __grid_constant__ CUtensorMap tm_b0, const __grid_constant__ CUtensorMap tm_b1,
                      const SearchParams p) {
+  // MODE 0: fp32 3xTF32 hi/lo; 4: raw fp32, ONE tf32 pass as a filter with a
+  // proven margin and exact fp32 rescoring of the survivors; 1/2: fp16/bf16
+  constexpr bool TF32 = (MODE == 0 || MODE == 4);
   constexpr int SPLIT = (MODE == 0) ? 2 : 1;
-  constexpr int BK = (MODE == 0) ? 32 : 64;  // elements per 128-byte K-chunk
-  constexpr uint32_t AB_FMT = (MODE == 0) ? 2u : (MODE == 1 ? 0u : 1u);
+  constexpr int BK = TF32 ? 32 : 64;  // elements per 128-byte K-chunk
+  constexpr uint32_t AB_FMT = TF32 ? 2u : (MODE == 1 ? 0u : 1u);
   // MODE 3 (bf16, L2): base rows are stored as [-2x | xn split in 3 bf16] and
   // query rows as [q | 1 1 1], so the accumulator already holds xn - 2 q.x and
   // the epilogue needs no base-norm tile (FOLD).
@@ -494,8 +498,9 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
                 } else {
 #pragma unroll
                   for (int kk = 0; kk < 4; ++kk) {
-                    if (kk >= nkk) break;
-                    mma_f16_ts(d_tmem, ah + 8 * kk, bd0 + 2 * kk, IDESC, (kb | kk) != 0);
+                    if (kk >= nkk) break;  // one K-step = 32 B of K = 8 TMEM columns (tf32 or 16-bit pairs)
+                    if (MODE == 4) mma_tf32_ts(d_tmem, ah + 8 * kk, bd0 + 2 * kk, IDESC, (kb | kk) != 0);
+                    else mma_f16_ts(d_tmem, ah + 8 * kk, bd0 + 2 * kk, IDESC, (kb | kk) != 0);
                   }
                 }
               } else {
@@ -516,7 +521,8 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
 #pragma unroll
                   for (int kk = 0; kk < 4; ++kk) {
                     if (kk >= nkk) break;
-                    mma_f16(d_tmem, ad0 + 2 * kk, bd0 + 2 * kk, IDESC, (kb | kk) != 0);
+                    if (MODE == 4) mma_tf32(d_tmem, ad0 + 2 * kk, bd0 + 2 * kk, IDESC, (kb | kk) != 0);
+                    else mma_f16(d_tmem, ad0 + 2 * kk, bd0 + 2 * kk, IDESC, (kb | kk) != 0);
                   }
                 }
               }
@@ -545,7 +551,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     const uint32_t lane_addr = static_cast<uint32_t>(eq * 32) << 16;
     const int k = p.k;
     const int dp = num_kb * BK;
-    const int a_cols = (MODE == 0) ? 2 * dp : dp / 2;  // TMEM columns of the query operand
+    const int a_cols = (MODE == 0) ? 2 * dp : (MODE == 4 ? dp : dp / 2);  // TMEM columns of the query operand
     uint32_t tcount = 0, a_buf = 0, a_ph = 0;
     uint32_t xs0 = 0, xp0 = 0, xs1 = 0, xp1 = 0;  // norm sub-ring positions (ring = tile % n_issuers)
     const uint32_t xh = (uint32_t)xn_slots / (uint32_t)p.n_issuers;
@@ -566,6 +572,8 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
           if (MODE == 0)
             src = (cc * 32 < dp) ? reinterpret_cast<const uint32_t*>(p.qa0) + (size_t)row * dp + cc * 32
                                  : reinterpret_cast<const uint32_t*>(p.qa1) + (size_t)row * dp + (cc * 32 - dp);
+          else if (MODE == 4)
+            src = reinterpret_cast<const uint32_t*>(p.qa0) + (size_t)row * dp + cc * 32;
           else
             src = reinterpret_cast<const uint32_t*>(p.qa0) + (size_t)row * (dp / 2) + cc * 32;
 #pragma unroll
@@ -586,7 +594,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       }
 
       constexpr bool RANGE = KQ < 0;
-      const float qn = ((!IS_IP || RANGE) && row_ok) ? p.qnorm[row] : 0.f;
+      const float qn = ((!IS_IP || RANGE || MODE == 4) && row_ok) ? p.qnorm[row] : 0.f;
       constexpr int KQS = KQ > 0 ? KQ : 1;
       uint32_t keys[KQS], pos[KQS];
       if constexpr (KQ > 0) {
@@ -614,8 +622,16 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       // Conservative fast-filter bound on f = fl(xn - 2ip): the reference value
       // fl(fl(qn + xn) - 2ip) differs from qn + f by < 3u(qn + xn + |v|); the
       // 2^-20 margin (u = 2^-24) over max-norm covers it with room to spare.
-      const float xmax = IS_IP ? 0.f : *p.xn_max;
+      const float xmax = (IS_IP && MODE != 4) ? 0.f : *p.xn_max;
+      // MODE 4: the single tf32 pass rounds each operand to 11 significant
+      // bits, |ip_tf32 - ip| <= 2^-9 sum|q_i||x_i| <= 2^-9 |q| |x|; the filter
+      // value f = xn - 2 ip moves by <= 2^-8 |q| max|x|.  Widen by 2^-7 (2x).
+      const float tf32_margin = (MODE == 4) ? 0.0078125f * sqrtf(fmaxf(qn, 0.f) * fmaxf(xmax, 0.f)) : 0.f;
       auto filter_bound = [&](float th) -> float {
+        if (MODE == 4) {
+          if (IS_IP) return th + 0.5f * tf32_margin;  // IP filters on -ip: half the L2 widening
+          return (th - qn) + (qn + xmax + fabsf(th)) * 9.5367431640625e-07f + tf32_margin;
+        }
         if (IS_IP) {
           // range search compares the GEMM inner product with the exact
           // direct one: widen by 2^-18 |q| max|x| (>> the 3xTF32 / fp32 error)
@@ -694,6 +710,19 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             }
           }
         };
+        auto exact_ip = [&](uint32_t position) -> float {
+          const float4* qv = reinterpret_cast<const float4*>(static_cast<const float*>(p.qa0) + (size_t)row * dp);
+          const float4* xv = reinterpret_cast<const float4*>(static_cast<const float*>(p.xbase) + (size_t)position * dp);
+          float acc = 0.f;
+          for (int i = 0; i < dp / 4; ++i) {
+            const float4 a = qv[i], b = __ldg(xv + i);
+            acc = fmaf(a.x, b.x, acc);
+            acc = fmaf(a.y, b.y, acc);
+            acc = fmaf(a.z, b.z, acc);
+            acc = fmaf(a.w, b.w, acc);
+          }
+          return acc;
+        };
         // rare path for one 32-column chunk: exact value + insertion per survivor
         auto slow_chunk = [&](const uint32_t (&r)[32], int c0) {
           float f[32];
@@ -721,7 +750,11 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
           while (cand) {
             const int j = __ffs(cand) - 1;
             cand &= cand - 1;
-            const float ip = select32(reinterpret_cast<const float(&)[32]>(r), j);
+            // MODE 4: the accumulator is the 1-pass tf32 filter value; the
+            // survivor's inner product is recomputed exactly in fp32 from the
+            // stored rows (sequential FMA over d, like an fp32 dot product)
+            const float ip = (MODE == 4) ? exact_ip(static_cast<uint32_t>(n0 + c0 + j))
+                                         : select32(reinterpret_cast<const float(&)[32]>(r), j);
             // flat.py:111: dmat = (qn + norms) - 2.0*ip  (2*ip exact -> one FMA;
             // FOLD: the accumulator already is xn - 2 ip)
             float v;
@@ -1156,6 +1189,9 @@ __global__ void prep_rows_kernel(const void* __restrict__ x, int in_dtype, int64
       static_cast<float*>(out0)[(size_t)orow * dp + c] = hi;
       static_cast<float*>(out1)[(size_t)orow * dp + c] = lo;
       acc += (double)v * (double)v;
+    } else if (MODE == 4) {  // raw fp32
+      static_cast<float*>(out0)[(size_t)orow * dp + c] = v;
+      acc += (double)v * (double)v;
     } else if (MODE == 1) {
       const __half h = __float2half_rn(v);
       static_cast<__half*>(out0)[(size_t)orow * dp + c] = h;
@@ -1197,6 +1233,8 @@ __global__ void reconstruct_kernel(const void* __restrict__ s0, const void* __re
     float v;
     if (MODE == 0)
       v = static_cast<const float*>(s0)[(size_t)r * dp + c] + static_cast<const float*>(s1)[(size_t)r * dp + c];
+    else if (MODE == 4)
+      v = static_cast<const float*>(s0)[(size_t)r * dp + c];
     else if (MODE == 1)
       v = __half2float(static_cast<const __half*>(s0)[(size_t)r * dp + c]);
     else
@@ -1262,6 +1300,7 @@ __global__ void range_exact_kernel(const unsigned long long* __restrict__ cand, 
   const uint32_t row = static_cast<uint32_t>(e >> 32), pos = static_cast<uint32_t>(e);
   auto val = [&](const void* a, const void* b, size_t off) -> double {
     if (MODE == 0) return (double)(static_cast<const float*>(a)[off] + static_cast<const float*>(b)[off]);
+    if (MODE == 4) return (double)static_cast<const float*>(a)[off];
     if (MODE == 1) return (double)__half2float(static_cast<const __half*>(a)[off]);
     return (double)__bfloat162float(static_cast<const __nv_bfloat16*>(a)[off]);
   };
