@@ -139,6 +139,7 @@ struct fk_index {
   int64_t* ids = nullptr;    // [cap]
   DevBuf q_in, q0, q1, qn, pkey, ppos, thr, pcnt, cbuf, fail, outD, outI, outP, stage_in, stage_ids;
   // range search: candidates, exact pass, sort scratch and the CSR result
+  DevBuf rfail, rcomp;  // fp32 MODE 4: per-query certification flags, exact-fallback composites
   DevBuf rcand, rcount, rdist, rkid, rkrd, rkeep, rrowc, rsel, rnsel, rtmp, rkid2, rkrd2, rv1, rv2, rlims, rids,
       rdist_out;
   float r_radius = 0.f;
@@ -729,6 +730,82 @@ int stage_queries(fk_index* h, const void* q, int64_t nq, int dtype, int on_devi
                      h->fold ? 2 : 0);
 }
 
+// fp32 MODE 4 search: fused pass with a 1-pass TF32 GEMM keeping k' >= k
+// entries per list in tf32 order, then merge_rescore_kernel (certify + exact
+// values + exact top-k); uncertified queries get the exact fallback.
+int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI, int64_t* dP, cudaEvent_t* ev,
+                 cudaStream_t st, Plan* plan_out) {
+  int rc;
+  // k' >= k entries per list, the slack absorbs the tf32 band around the k-th
+  const int kp = k <= 16 ? 32 : std::min(k + std::max(64, k / 4), FK_MAX_K);
+  const int kq = kp <= 32 ? 32 : 0;
+  Plan pl;
+  if ((rc = make_plan(h, nq, h->ntotal, kp, kq, 0, &pl))) return rc;
+  *plan_out = pl;
+  if ((rc = h->thr.ensure((size_t)nq * sizeof(uint32_t)))) return rc;
+  CK(cudaMemsetAsync(h->thr.p, 0xFF, (size_t)nq * sizeof(uint32_t), st));
+  if (ev) CK(cudaEventRecord(ev[1], st));
+  if ((rc = run_fused(h, pl, nq, h->ntotal, kp, ip, st))) return rc;
+  if (ev) CK(cudaEventRecord(ev[2], st));
+  if ((rc = h->rfail.ensure((size_t)nq * sizeof(int)))) return rc;
+  const int smc = std::min(MERGE_SMC, std::max(1024, 8 * kp));
+  int p2 = 1;
+  while (p2 < k) p2 <<= 1;
+  static bool cfg = false;
+  if (!cfg) {
+    CK(cudaFuncSetAttribute(merge_rescore_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (MERGE_SMC + FK_MAX_K) * 8));
+    CK(cudaFuncSetAttribute(merge_rescore_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (MERGE_SMC + FK_MAX_K) * 8));
+    CK(cudaFuncSetAttribute(select_topk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, FK_MAX_K * 8));
+    CK(cudaFuncSetAttribute(select_topk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, FK_MAX_K * 8));
+    cfg = true;
+  }
+  const size_t msmem = (size_t)(smc + p2) * 8;
+  const auto pk = static_cast<const uint32_t*>(h->pkey.p);
+  const auto pp = static_cast<const uint32_t*>(h->ppos.p);
+  const int* pc = kq == 0 ? static_cast<const int*>(h->pcnt.p) : nullptr;
+  const auto thr = static_cast<const uint32_t*>(h->thr.p);
+  const auto q0 = static_cast<const float*>(h->q0.p);
+  const auto xb = static_cast<const float*>(h->s0);
+  const auto qn = static_cast<const float*>(h->qn.p);
+  int* fail = static_cast<int*>(h->rfail.p);
+  if (ip)
+    merge_rescore_kernel<true><<<(unsigned)nq, 256, msmem, st>>>(pk, pp, pc, pl.S_tot, (int)nq, kp, k, thr, q0, xb, qn,
+                                                                  h->norms, h->xn_max, h->dp, h->ids, dD, dI, dP, smc,
+                                                                  fail);
+  else
+    merge_rescore_kernel<false><<<(unsigned)nq, 256, msmem, st>>>(pk, pp, pc, pl.S_tot, (int)nq, kp, k, thr, q0, xb, qn,
+                                                                   h->norms, h->xn_max, h->dp, h->ids, dD, dI, dP, smc,
+                                                                   fail);
+  CKL();
+  h->nlaunch++;
+  std::vector<int> hf((size_t)nq);
+  CK(cudaMemcpyAsync(hf.data(), fail, (size_t)nq * sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  int64_t nfail = 0;
+  for (int64_t i = 0; i < nq; ++i) {
+    if (!hf[i]) continue;
+    ++nfail;
+    if ((rc = h->rcomp.ensure((size_t)h->ntotal * 8))) return rc;
+    auto comp = static_cast<uint64_t*>(h->rcomp.p);
+    const unsigned g = (unsigned)((h->ntotal + 255) / 256);
+    if (ip) exact_all_kernel<true><<<g, 256, 0, st>>>(q0 + (size_t)i * h->dp, qn + i, xb, h->norms, h->ntotal, h->dp, comp);
+    else exact_all_kernel<false><<<g, 256, 0, st>>>(q0 + (size_t)i * h->dp, qn + i, xb, h->norms, h->ntotal, h->dp, comp);
+    CKL();
+    const size_t ssm = (size_t)p2 * 8;
+    if (ip)
+      select_topk_kernel<true><<<1, 256, ssm, st>>>(comp, h->ntotal, k, h->ids, dD + i * k, dI + i * k,
+                                                    dP ? dP + i * k : nullptr);
+    else
+      select_topk_kernel<false><<<1, 256, ssm, st>>>(comp, h->ntotal, k, h->ids, dD + i * k, dI + i * k,
+                                                     dP ? dP + i * k : nullptr);
+    CKL();
+  }
+  h->est_fallbacks += nfail;
+  return FK_OK;
+}
+
 __global__ void gather_range_kernel(const unsigned int* __restrict__ order, const unsigned long long* __restrict__ key_id,
                                     const float* __restrict__ dist, int64_t n, int64_t* __restrict__ ids_out,
                                     float* __restrict__ dist_out) {
@@ -934,6 +1011,24 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
                                                                          ip ? -INFINITY : INFINITY);
     CKL();
     h->nlaunch = 1;
+  } else if (kmode_of(h) == 4) {
+    if (ev) CK(cudaEventRecord(ev[0], st));
+    if ((rc = stage_queries(h, q, nq, dtype, on_device, st))) return rc;
+    h->nlaunch++;
+    Plan pl;
+    if ((rc = search_mode4(h, nq, k, ip, dD, dI, dP, ev, st, &pl))) return rc;
+    if (ev) CK(cudaEventRecord(ev[3], st));
+    h->plan[0] = pl.grid;
+    h->plan[1] = pl.S;
+    h->plan[2] = pl.chunk_tiles;
+    h->plan[3] = pl.num_units;
+    h->plan[4] = pl.stages;
+    h->plan[5] = pl.a_mode;
+    h->plan[6] = pl.smem;
+    h->plan[7] = pl.kq * 100 + pl.epi;
+    h->plan[8] = pl.acc_stages;
+    h->plan[9] = pl.epi;
+    h->plan[10] = pl.bn;
   } else {
     const int kq = k <= 8 ? 8 : k <= 16 ? 16 : k <= 32 ? 32 : 0;  // 0: large-k buffers
 

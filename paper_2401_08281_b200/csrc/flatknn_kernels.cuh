@@ -623,12 +623,14 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       // fl(fl(qn + xn) - 2ip) differs from qn + f by < 3u(qn + xn + |v|); the
       // 2^-20 margin (u = 2^-24) over max-norm covers it with room to spare.
       const float xmax = (IS_IP && MODE != 4) ? 0.f : *p.xn_max;
-      // MODE 4: the single tf32 pass rounds each operand to 11 significant
-      // bits, |ip_tf32 - ip| <= 2^-9 sum|q_i||x_i| <= 2^-9 |q| |x|; the filter
-      // value f = xn - 2 ip moves by <= 2^-8 |q| max|x|.  Widen by 2^-7 (2x).
-      const float tf32_margin = (MODE == 4) ? 0.0078125f * sqrtf(fmaxf(qn, 0.f) * fmaxf(xmax, 0.f)) : 0.f;
+      // MODE 4 range search: the single tf32 pass rounds each operand to 11
+      // significant bits, |ip_tf32 - ip| <= 2^-9 sum|q_i||x_i| <= 2^-9 |q||x|,
+      // so f = xn - 2 ip moves by <= 2^-8 |q| max|x|: widen by 2^-7 (2x) before
+      // the exact direct-distance pass.  (Top-k queues stay in tf32 space.)
+      const float tf32_margin =
+          (MODE == 4 && RANGE) ? 0.0078125f * sqrtf(fmaxf(qn, 0.f) * fmaxf(xmax, 0.f)) : 0.f;
       auto filter_bound = [&](float th) -> float {
-        if (MODE == 4) {
+        if (MODE == 4 && RANGE) {
           if (IS_IP) return th + 0.5f * tf32_margin;  // IP filters on -ip: half the L2 widening
           return (th - qn) + (qn + xmax + fabsf(th)) * 9.5367431640625e-07f + tf32_margin;
         }
@@ -710,19 +712,6 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             }
           }
         };
-        auto exact_ip = [&](uint32_t position) -> float {
-          const float4* qv = reinterpret_cast<const float4*>(static_cast<const float*>(p.qa0) + (size_t)row * dp);
-          const float4* xv = reinterpret_cast<const float4*>(static_cast<const float*>(p.xbase) + (size_t)position * dp);
-          float acc = 0.f;
-          for (int i = 0; i < dp / 4; ++i) {
-            const float4 a = qv[i], b = __ldg(xv + i);
-            acc = fmaf(a.x, b.x, acc);
-            acc = fmaf(a.y, b.y, acc);
-            acc = fmaf(a.z, b.z, acc);
-            acc = fmaf(a.w, b.w, acc);
-          }
-          return acc;
-        };
         // rare path for one 32-column chunk: exact value + insertion per survivor
         auto slow_chunk = [&](const uint32_t (&r)[32], int c0) {
           float f[32];
@@ -750,11 +739,9 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
           while (cand) {
             const int j = __ffs(cand) - 1;
             cand &= cand - 1;
-            // MODE 4: the accumulator is the 1-pass tf32 filter value; the
-            // survivor's inner product is recomputed exactly in fp32 from the
-            // stored rows (sequential FMA over d, like an fp32 dot product)
-            const float ip = (MODE == 4) ? exact_ip(static_cast<uint32_t>(n0 + c0 + j))
-                                         : select32(reinterpret_cast<const float(&)[32]>(r), j);
+            // (MODE 4: a 1-pass tf32 value; the queue works in that space and
+            // merge_rescore_kernel recomputes the survivors exactly)
+            const float ip = select32(reinterpret_cast<const float(&)[32]>(r), j);
             // flat.py:111: dmat = (qn + norms) - 2.0*ip  (2*ip exact -> one FMA;
             // FOLD: the accumulator already is xn - 2 ip)
             float v;
@@ -1150,6 +1137,227 @@ __global__ void __launch_bounds__(256) merge_large_kernel(const uint32_t* __rest
       D[o] = IS_IP ? -v : v;
       I[o] = ids[ps];
       if (P) P[o] = ps;
+    }
+  }
+}
+
+// ------------------------------------------------------------ MODE 4 rescoring merge
+// fp32 MODE 4 runs the fused pass with a 1-pass TF32 GEMM and keeps k' >= k
+// entries per list ranked by their tf32 value t.  With e = max|t - v| over all
+// pairs (|t - v| <= 2^-8 |q| max|x| for L2, half for IP), every exact top-k
+// member has t <= t_k + 2e (t_k = k-th smallest t overall), and every entry
+// that did not reach a list has t >= bound (the final shared k'-th bound).
+// One CTA per query: gather the list entries below the bound, CERTIFY
+// bound > t_k + 2e (else flag the query for the exact fallback), recompute the
+// gathered entries' distances exactly (fp32 FMA over d from the stored rows,
+// the value of flat.py:111) and select the exact top-k by (value, position).
+template <bool IS_IP>
+__global__ void __launch_bounds__(256) merge_rescore_kernel(
+    const uint32_t* __restrict__ pkey, const uint32_t* __restrict__ ppos, const int* __restrict__ pcnt, int S, int nq,
+    int kp, int k, const uint32_t* __restrict__ thr_key, const float* __restrict__ q0, const float* __restrict__ xb,
+    const float* __restrict__ qnorm, const float* __restrict__ xnorm, const float* __restrict__ xn_max, int dp,
+    const int64_t* __restrict__ ids, float* __restrict__ D, int64_t* __restrict__ I, int64_t* __restrict__ P, int smc,
+    int* __restrict__ fail) {
+  extern __shared__ uint64_t sm[];  // smc gathered entries, then the k winners (pow2-padded)
+  __shared__ int count, count2;
+  __shared__ uint32_t hist[256], sel[8];
+  const int q = blockIdx.x;
+  const int tid = threadIdx.x;
+  if (q >= nq) return;
+  const uint32_t thr = thr_key[q];
+  const uint32_t* lk = pkey + (size_t)q * S * kp;
+  const uint32_t* lp = ppos + (size_t)q * S * kp;
+  const int* lc = pcnt ? pcnt + (size_t)q * S : nullptr;
+  if (tid == 0) {
+    count = 0;
+    count2 = 0;
+  }
+  __syncthreads();
+  const int total = S * kp;
+  for (int e = tid; e < total; e += blockDim.x) {
+    const uint32_t key = lk[e];
+    if (key > thr) continue;
+    const uint32_t ps = lp[e];
+    if (ps == 0xFFFFFFFFu) continue;
+    if (lc) {
+      const int s = e / kp;
+      if (e - s * kp >= lc[s]) continue;
+    }
+    const int idx = atomicAdd(&count, 1);
+    if (idx < smc) sm[idx] = (static_cast<uint64_t>(key) << 32) | ps;
+  }
+  __syncthreads();
+  const int n = count;
+  if (n > smc) {  // more survivors than the buffer: exact fallback for this query
+    if (tid == 0) fail[q] = 1;
+    return;
+  }
+  // certification on the tf32 values
+  const float qn = qnorm[q];
+  // band 2e with a 2x safety factor: L2 2 * 2 * 2^-8, IP 2 * 2 * 2^-9 (|q| max|x|)
+  const float e2 = (IS_IP ? 0.0078125f : 0.015625f) * sqrtf(fmaxf(qn, 0.f) * fmaxf(*xn_max, 0.f));
+  bool ok = true;
+  if (thr != 0xFFFFFFFFu && n >= k) {
+    const uint64_t kth = block_kth([&](int e) { return sm[e]; }, n, (uint32_t)k, hist, sel);
+    const float tk = unmonotone(static_cast<uint32_t>(kth >> 32));
+    const float b = unmonotone(thr);
+    ok = b > tk + e2 + 9.5367431640625e-07f * (fabsf(tk) + qn);
+  } else if (thr != 0xFFFFFFFFu) {
+    ok = false;  // fewer than k gathered although entries were dropped
+  }
+  if (tid == 0) fail[q] = ok ? 0 : 1;
+  if (!ok) return;
+  // exact values for the gathered entries
+  const float4* qv = reinterpret_cast<const float4*>(q0 + (size_t)q * dp);
+  for (int i = tid; i < n; i += blockDim.x) {
+    const uint32_t ps = static_cast<uint32_t>(sm[i]);
+    const float4* xv = reinterpret_cast<const float4*>(xb + (size_t)ps * dp);
+    float acc = 0.f;
+    for (int c = 0; c < dp / 4; ++c) {
+      const float4 a = __ldg(qv + c), bb = __ldg(xv + c);
+      acc = fmaf(a.x, bb.x, acc);
+      acc = fmaf(a.y, bb.y, acc);
+      acc = fmaf(a.z, bb.z, acc);
+      acc = fmaf(a.w, bb.w, acc);
+    }
+    float v;
+    if (IS_IP) v = -acc;
+    else {
+      v = fmaf(-2.f, acc, qn + xnorm[ps]);  // flat.py:111
+      v = (v <= 0.f) ? 0.f : v;              // flat.py:112
+    }
+    sm[i] = (static_cast<uint64_t>(monotone(v)) << 32) | ps;
+  }
+  __syncthreads();
+  uint64_t* win = sm + smc;
+  int nw;
+  if (n <= k) {
+    for (int i = tid; i < n; i += blockDim.x) win[i] = sm[i];
+    nw = n;
+  } else {
+    const uint64_t kth = block_kth([&](int e) { return sm[e]; }, n, (uint32_t)k, hist, sel);
+    for (int i = tid; i < n; i += blockDim.x)
+      if (sm[i] <= kth) win[atomicAdd(&count2, 1)] = sm[i];
+    __syncthreads();
+    nw = count2;
+  }
+  int P2 = 1;
+  while (P2 < nw) P2 <<= 1;
+  for (int i = nw + tid; i < P2; i += blockDim.x) win[i] = ~0ull;
+  __syncthreads();
+  for (int size = 2; size <= P2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = tid; i < P2 / 2; i += blockDim.x) {
+        const int lo = 2 * i - (i & (stride - 1));
+        const int hi = lo + stride;
+        const bool asc = (lo & size) == 0;
+        const uint64_t a = win[lo], b2 = win[hi];
+        if ((a > b2) == asc) {
+          win[lo] = b2;
+          win[hi] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int r = tid; r < k; r += blockDim.x) {
+    const size_t o = (size_t)q * k + r;
+    const uint64_t w = r < nw ? win[r] : ~0ull;
+    if (w == ~0ull) {
+      D[o] = IS_IP ? -INFINITY : INFINITY;
+      I[o] = -1;
+      if (P) P[o] = -1;
+    } else {
+      const uint32_t ps = static_cast<uint32_t>(w);
+      const float v = unmonotone(static_cast<uint32_t>(w >> 32));
+      D[o] = IS_IP ? -v : v;
+      I[o] = ids[ps];
+      if (P) P[o] = ps;
+    }
+  }
+}
+
+// Exact fallback for one query (uncertified in merge_rescore_kernel): the
+// exact (value, position) composite of every stored row.
+template <bool IS_IP>
+__global__ void exact_all_kernel(const float* __restrict__ qrow, const float* __restrict__ qn_ptr, const float* __restrict__ xb,
+                                 const float* __restrict__ xnorm, int64_t n, int dp, uint64_t* __restrict__ out) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const float qn = *qn_ptr;
+  const float4* qv = reinterpret_cast<const float4*>(qrow);
+  const float4* xv = reinterpret_cast<const float4*>(xb + (size_t)r * dp);
+  float acc = 0.f;
+  for (int c = 0; c < dp / 4; ++c) {
+    const float4 a = __ldg(qv + c), b = __ldg(xv + c);
+    acc = fmaf(a.x, b.x, acc);
+    acc = fmaf(a.y, b.y, acc);
+    acc = fmaf(a.z, b.z, acc);
+    acc = fmaf(a.w, b.w, acc);
+  }
+  float v;
+  if (IS_IP) v = -acc;
+  else {
+    v = fmaf(-2.f, acc, qn + xnorm[r]);
+    v = (v <= 0.f) ? 0.f : v;
+  }
+  out[r] = (static_cast<uint64_t>(monotone(v)) << 32) | static_cast<uint32_t>(r);
+}
+
+// Exact top-k of n composites in global memory (one CTA): radix select + sort.
+template <bool IS_IP>
+__global__ void __launch_bounds__(256) select_topk_kernel(const uint64_t* __restrict__ comp, int64_t n, int k,
+                                                          const int64_t* __restrict__ ids, float* __restrict__ D,
+                                                          int64_t* __restrict__ I, int64_t* __restrict__ P) {
+  extern __shared__ uint64_t win[];
+  __shared__ int count;
+  __shared__ uint32_t hist[256], sel[8];
+  const int tid = threadIdx.x;
+  if (tid == 0) count = 0;
+  __syncthreads();
+  const int nn = (int)n;
+  int nw;
+  if (nn <= k) {
+    for (int i = tid; i < nn; i += blockDim.x) win[i] = comp[i];
+    nw = nn;
+  } else {
+    const uint64_t kth = block_kth([&](int e) { return comp[e]; }, nn, (uint32_t)k, hist, sel);
+    for (int i = tid; i < nn; i += blockDim.x)
+      if (comp[i] <= kth) win[atomicAdd(&count, 1)] = comp[i];
+    __syncthreads();
+    nw = count;
+  }
+  int P2 = 1;
+  while (P2 < nw) P2 <<= 1;
+  for (int i = nw + tid; i < P2; i += blockDim.x) win[i] = ~0ull;
+  __syncthreads();
+  for (int size = 2; size <= P2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = tid; i < P2 / 2; i += blockDim.x) {
+        const int lo = 2 * i - (i & (stride - 1));
+        const int hi = lo + stride;
+        const bool asc = (lo & size) == 0;
+        const uint64_t a = win[lo], b = win[hi];
+        if ((a > b) == asc) {
+          win[lo] = b;
+          win[hi] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int r = tid; r < k; r += blockDim.x) {
+    const uint64_t w = r < nw ? win[r] : ~0ull;
+    if (w == ~0ull) {
+      D[r] = IS_IP ? -INFINITY : INFINITY;
+      I[r] = -1;
+      if (P) P[r] = -1;
+    } else {
+      const uint32_t ps = static_cast<uint32_t>(w);
+      const float v = unmonotone(static_cast<uint32_t>(w >> 32));
+      D[r] = IS_IP ? -v : v;
+      I[r] = ids[ps];
+      if (P) P[r] = ps;
     }
   }
 }

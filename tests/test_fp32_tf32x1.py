@@ -1,0 +1,74 @@
+"""Experimental fp32 algorithm (FK_FP32_ALGO=1, kernel MODE 4): raw fp32
+storage, ONE tf32 tensor-core pass ranking k' >= k candidates per list, then
+certification (tf32 error band) + exact fp32 rescoring of the survivors, with
+an exact brute-force fallback for uncertified queries.  Must return the same
+answers as the default 3xTF32 path under the north-star parity rules."""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+sys.path.insert(0, os.path.join(HERE, "golden"))
+sys.path.insert(0, os.path.dirname(HERE))
+
+from cases import CASES, make_inputs  # noqa: E402
+from oracle import flat_oracle as O  # noqa: E402
+from parity import assert_parity  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+GOLD = np.load(os.path.join(HERE, "golden", "golden.npz"))
+
+
+def _index(d, metric):
+    from paper_2401_08281_b200 import METRIC_IP, METRIC_L2, FlatIndex
+    os.environ["FK_FP32_ALGO"] = "1"
+    try:
+        return FlatIndex(d, METRIC_IP if metric == "ip" else METRIC_L2, storage="fp32")
+    finally:
+        del os.environ["FK_FP32_ALGO"]
+
+
+FP32_CASES = [n for n in CASES if make_inputs(n)[4] == "fp32"]
+
+
+@pytest.mark.parametrize("name", FP32_CASES)
+def test_tf32x1_golden(name):
+    xb, q, k, metric, storage, ids = make_inputs(name)
+    idx = _index(xb.shape[1], metric)
+    if xb.shape[0]:
+        if ids is None:
+            idx.add(xb)
+        else:
+            idx.add_with_ids(xb, ids)
+    res = idx.search(q, k)
+    assert_parity(res.ids, res.distances, GOLD[f"{name}/blas_ids"], GOLD[f"{name}/blas_dist"])
+
+
+@pytest.mark.parametrize("metric", ["l2", "ip"])
+@pytest.mark.parametrize("k", [1, 10, 16, 32, 100])
+def test_tf32x1_vs_oracle(metric, k):
+    rng = np.random.default_rng(99 + k)
+    xb = rng.standard_normal((60000, 64), dtype=np.float32)
+    q = rng.standard_normal((300, 64), dtype=np.float32)
+    idx = _index(64, metric)
+    idx.add(xb)
+    res = idx.search(q, k)
+    want_ids, want_dist = O.flat_search_blas(xb, q, k, metric)
+    assert_parity(res.ids, res.distances, want_ids, want_dist)
+
+
+def test_tf32x1_exact_ties_use_the_certified_fallback():
+    """Integer data with massive exact ties: the band test cannot certify the
+    queries, the exact fallback must reproduce the reference order exactly."""
+    rng = np.random.default_rng(3)
+    xb = rng.integers(0, 3, size=(5000, 16)).astype(np.float32)
+    q = rng.integers(0, 3, size=(20, 16)).astype(np.float32)
+    idx = _index(16, "l2")
+    idx.add(xb)
+    res = idx.search(q, 10)
+    want_ids, want_dist = O.flat_search_blas(xb, q, 10, "l2")
+    assert np.array_equal(res.ids, want_ids)
+    assert np.array_equal(res.distances, want_dist)
