@@ -93,6 +93,10 @@ int make_map(CUtensorMap* m, const void* base, int elem_bytes, uint64_t cols, ui
 }
 
 constexpr int FK_MAX_K = 2048;
+// fp32 searches with k <= 16 over at least this many rows run the 1-pass TF32
+// filter + exact rescoring (kmode 4) on the hi half of the split storage;
+// smaller searches are dominated by the rescoring merge and keep 3xTF32
+constexpr int64_t FP32_1X_MIN_ROWS = 262144;
 constexpr size_t L2_CHUNK_BYTES = 48ull << 20;  // streamed base per N-chunk (2 chunks in flight << 126 MB L2)
 constexpr size_t PARTIAL_BYTES = 4ull << 30;    // split-N partial top-k lists
 constexpr int MERGE_SMC = 16384;    // large-k merge: survivors gathered in smem (128 KB) + 2048 winners
@@ -487,11 +491,14 @@ namespace {
 
 struct Plan {
   int kq, epi, nh, num_m, n_tiles, S, chunk_tiles, num_units, grid, a_mode, stages, smem, S_tot, cap, xn_slots,
-      acc_stages, n_issuers, cluster, num_mu, bn;
+      acc_stages, n_issuers, cluster, num_mu, bn, kmode;
 };
 
 // Tile / split-N / pipeline plan for one fused pass over base rows [0, nb_pass).
-int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force_S, Plan* pl) {
+// kmode: kernel operand mode of this pass (-1: the index's own); fp32
+// storage runs either 3xTF32 (kmode 0, hi+lo streamed) or the 1-pass TF32
+// filter (kmode 4, hi or raw streamed)
+int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force_S, Plan* pl, int kmode = -1) {
   Plan P{};
   P.kq = kq;
   // 16-bit storage: 2 epilogue warps per TMEM lane quarter (the epilogue, not
@@ -500,7 +507,9 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   if (const char* e = getenv("FK_EPI"); e && kq >= 0) P.epi = atoi(e) == 8 ? 8 : 4;
   P.nh = P.epi / 4;
   P.num_m = (int)((nq + BM - 1) / BM);
-  const int split = h->split;
+  if (kmode < 0) kmode = kmode_of(h);
+  P.kmode = kmode;
+  const int split = kmode == 0 ? 2 : 1;
   const int num_kb = h->dp / chunk_elems_of(h->storage);
   const int a_bytes = split * num_kb * (int)CHUNK_BYTES;
   const int a_tmem_cols = h->storage == FK_F32 ? split * h->dp : h->dp / 2;
@@ -539,7 +548,7 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   if (P.num_m < 2 || h->num_sms < 2) P.cluster = 1;
   P.num_mu = (P.num_m + P.cluster - 1) / P.cluster;
   // chunk <= L2_CHUNK_BYTES of streamed base; partial lists <= PARTIAL_BYTES
-  const size_t tile_bytes = (size_t)bn * h->dp * elem_bytes_of(h->storage) * h->split;
+  const size_t tile_bytes = (size_t)bn * h->dp * elem_bytes_of(h->storage) * split;
   // (very large k: partial lists are k deep, so merge cost grows with S -> 4x window)
   size_t l2_chunk = L2_CHUNK_BYTES;
   if (const char* e = getenv("FK_L2_CHUNK_MB")) l2_chunk = (size_t)std::max(1, atoi(e)) << 20;
@@ -612,7 +621,7 @@ int run_fused(fk_index* h, const Plan& P, int64_t nq, int64_t nb_pass, int k, bo
   if ((rc = make_map(&ta0, h->q0.p, eb, h->dp, nq))) return rc;
   const uint32_t b_rows = P.cluster == 2 ? P.bn / 2 : P.bn;  // cluster mode: each CTA loads half a tile
   if ((rc = make_map(&tb0, h->s0, eb, h->dp, nb_pass, b_rows))) return rc;
-  if (h->split == 2) {
+  if (P.kmode == 0) {
     if ((rc = make_map(&ta1, h->q1.p, eb, h->dp, nq))) return rc;
     if ((rc = make_map(&tb1, h->s1, eb, h->dp, nb_pass, b_rows))) return rc;
   } else {
@@ -665,7 +674,7 @@ int run_fused(fk_index* h, const Plan& P, int64_t nq, int64_t nb_pass, int k, bo
   sp.num_mu = P.num_mu;
   if (const char* e = getenv("FK_DEBUG_FLAGS")) sp.dbg_flags = atoi(e);
   if (const char* e = getenv("FK_B_POLICY")) sp.b_policy = atoi(e);
-  rc = launch_fused(P.epi, kmode_of(h), h->fold != 0, ip, P.kq, ta0, ta1, tb0, tb1, sp, P.grid, P.smem, st);
+  rc = launch_fused(P.epi, P.kmode, h->fold != 0, ip, P.kq, ta0, ta1, tb0, tb1, sp, P.grid, P.smem, st);
   if (rc == FK_OK) h->nlaunch++;
   return rc;
 }
@@ -740,7 +749,7 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
   const int kp = k <= 16 ? 32 : std::min(k + std::max(64, k / 4), FK_MAX_K);
   const int kq = kp <= 32 ? 32 : 0;
   Plan pl;
-  if ((rc = make_plan(h, nq, h->ntotal, kp, kq, 0, &pl))) return rc;
+  if ((rc = make_plan(h, nq, h->ntotal, kp, kq, 0, &pl, 4))) return rc;
   *plan_out = pl;
   if ((rc = h->thr.ensure((size_t)nq * sizeof(uint32_t)))) return rc;
   CK(cudaMemsetAsync(h->thr.p, 0xFF, (size_t)nq * sizeof(uint32_t), st));
@@ -768,14 +777,17 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
   const auto thr = static_cast<const uint32_t*>(h->thr.p);
   const auto q0 = static_cast<const float*>(h->q0.p);
   const auto xb = static_cast<const float*>(h->s0);
+  // split storage: the exact operands are hi + lo (exact in fp32)
+  const auto q1 = h->split == 2 ? static_cast<const float*>(h->q1.p) : nullptr;
+  const auto xl = h->split == 2 ? static_cast<const float*>(h->s1) : nullptr;
   const auto qn = static_cast<const float*>(h->qn.p);
   int* fail = static_cast<int*>(h->rfail.p);
   if (ip)
-    merge_rescore_kernel<true><<<(unsigned)nq, 256, msmem, st>>>(pk, pp, pc, pl.S_tot, (int)nq, kp, k, thr, q0, xb, qn,
+    merge_rescore_kernel<true><<<(unsigned)nq, 256, msmem, st>>>(pk, pp, pc, pl.S_tot, (int)nq, kp, k, thr, q0, q1, xb, xl, qn,
                                                                   h->norms, h->xn_max, h->dp, h->ids, dD, dI, dP, smc,
                                                                   fail);
   else
-    merge_rescore_kernel<false><<<(unsigned)nq, 256, msmem, st>>>(pk, pp, pc, pl.S_tot, (int)nq, kp, k, thr, q0, xb, qn,
+    merge_rescore_kernel<false><<<(unsigned)nq, 256, msmem, st>>>(pk, pp, pc, pl.S_tot, (int)nq, kp, k, thr, q0, q1, xb, xl, qn,
                                                                    h->norms, h->xn_max, h->dp, h->ids, dD, dI, dP, smc,
                                                                    fail);
   CKL();
@@ -790,8 +802,13 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
     if ((rc = h->rcomp.ensure((size_t)h->ntotal * 8))) return rc;
     auto comp = static_cast<uint64_t*>(h->rcomp.p);
     const unsigned g = (unsigned)((h->ntotal + 255) / 256);
-    if (ip) exact_all_kernel<true><<<g, 256, 0, st>>>(q0 + (size_t)i * h->dp, qn + i, xb, h->norms, h->ntotal, h->dp, comp);
-    else exact_all_kernel<false><<<g, 256, 0, st>>>(q0 + (size_t)i * h->dp, qn + i, xb, h->norms, h->ntotal, h->dp, comp);
+    const float* qlo = q1 ? q1 + (size_t)i * h->dp : nullptr;
+    if (ip)
+      exact_all_kernel<true><<<g, 256, 0, st>>>(q0 + (size_t)i * h->dp, qlo, qn + i, xb, xl, h->norms, h->ntotal, h->dp,
+                                                comp);
+    else
+      exact_all_kernel<false><<<g, 256, 0, st>>>(q0 + (size_t)i * h->dp, qlo, qn + i, xb, xl, h->norms, h->ntotal,
+                                                 h->dp, comp);
     CKL();
     const size_t ssm = (size_t)p2 * 8;
     if (ip)
@@ -1011,7 +1028,8 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
                                                                          ip ? -INFINITY : INFINITY);
     CKL();
     h->nlaunch = 1;
-  } else if (kmode_of(h) == 4) {
+  } else if (h->storage == FK_F32 &&
+             (h->split == 1 || (k <= 16 && h->ntotal >= FP32_1X_MIN_ROWS && !getenv("FK_FP32_3X")))) {
     if (ev) CK(cudaEventRecord(ev[0], st));
     if ((rc = stage_queries(h, q, nq, dtype, on_device, st))) return rc;
     h->nlaunch++;

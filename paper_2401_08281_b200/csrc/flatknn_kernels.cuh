@@ -1142,6 +1142,29 @@ __global__ void __launch_bounds__(256) merge_large_kernel(const uint32_t* __rest
 }
 
 // ------------------------------------------------------------ MODE 4 rescoring merge
+// Exact fp32 inner product over dp (sequential FMA, the order of an fp32 dot
+// product); the operands are hi (+ lo when the storage is split: hi + lo == x
+// exactly in fp32).
+__device__ __forceinline__ float exact_dot(const float4* __restrict__ qh, const float4* __restrict__ ql,
+                                           const float4* __restrict__ xh, const float4* __restrict__ xl, int dp) {
+  float acc = 0.f;
+  for (int c = 0; c < dp / 4; ++c) {
+    float4 a = __ldg(qh + c), b = __ldg(xh + c);
+    if (ql) {
+      const float4 t = __ldg(ql + c);
+      a = make_float4(a.x + t.x, a.y + t.y, a.z + t.z, a.w + t.w);
+    }
+    if (xl) {
+      const float4 t = __ldg(xl + c);
+      b = make_float4(b.x + t.x, b.y + t.y, b.z + t.z, b.w + t.w);
+    }
+    acc = fmaf(a.x, b.x, acc);
+    acc = fmaf(a.y, b.y, acc);
+    acc = fmaf(a.z, b.z, acc);
+    acc = fmaf(a.w, b.w, acc);
+  }
+  return acc;
+}
 // fp32 MODE 4 runs the fused pass with a 1-pass TF32 GEMM and keeps k' >= k
 // entries per list ranked by their tf32 value t.  With e = max|t - v| over all
 // pairs (|t - v| <= 2^-8 |q| max|x| for L2, half for IP), every exact top-k
@@ -1154,7 +1177,8 @@ __global__ void __launch_bounds__(256) merge_large_kernel(const uint32_t* __rest
 template <bool IS_IP>
 __global__ void __launch_bounds__(256) merge_rescore_kernel(
     const uint32_t* __restrict__ pkey, const uint32_t* __restrict__ ppos, const int* __restrict__ pcnt, int S, int nq,
-    int kp, int k, const uint32_t* __restrict__ thr_key, const float* __restrict__ q0, const float* __restrict__ xb,
+    int kp, int k, const uint32_t* __restrict__ thr_key, const float* __restrict__ q0, const float* __restrict__ q1,
+    const float* __restrict__ xb, const float* __restrict__ xl,
     const float* __restrict__ qnorm, const float* __restrict__ xnorm, const float* __restrict__ xn_max, int dp,
     const int64_t* __restrict__ ids, float* __restrict__ D, int64_t* __restrict__ I, int64_t* __restrict__ P, int smc,
     int* __restrict__ fail) {
@@ -1187,7 +1211,7 @@ __global__ void __launch_bounds__(256) merge_rescore_kernel(
     if (idx < smc) sm[idx] = (static_cast<uint64_t>(key) << 32) | ps;
   }
   __syncthreads();
-  const int n = count;
+  int n = count;
   if (n > smc) {  // more survivors than the buffer: exact fallback for this query
     if (tid == 0) fail[q] = 1;
     return;
@@ -1197,29 +1221,45 @@ __global__ void __launch_bounds__(256) merge_rescore_kernel(
   // band 2e with a 2x safety factor: L2 2 * 2 * 2^-8, IP 2 * 2 * 2^-9 (|q| max|x|)
   const float e2 = (IS_IP ? 0.0078125f : 0.015625f) * sqrtf(fmaxf(qn, 0.f) * fmaxf(*xn_max, 0.f));
   bool ok = true;
-  if (thr != 0xFFFFFFFFu && n >= k) {
+  uint32_t band_key = 0xFFFFFFFFu;  // only entries with t <= t_k + band can be in the exact top-k
+  if (n >= k) {
     const uint64_t kth = block_kth([&](int e) { return sm[e]; }, n, (uint32_t)k, hist, sel);
     const float tk = unmonotone(static_cast<uint32_t>(kth >> 32));
-    const float b = unmonotone(thr);
-    ok = b > tk + e2 + 9.5367431640625e-07f * (fabsf(tk) + qn);
+    const float lim = tk + e2 + 9.5367431640625e-07f * (fabsf(tk) + qn);
+    band_key = monotone(lim);
+    if (thr != 0xFFFFFFFFu) ok = unmonotone(thr) > lim;
   } else if (thr != 0xFFFFFFFFu) {
     ok = false;  // fewer than k gathered although entries were dropped
   }
   if (tid == 0) fail[q] = ok ? 0 : 1;
   if (!ok) return;
-  // exact values for the gathered entries
+  // keep the band only (typically k + a few): in-place compaction
+  if (band_key != 0xFFFFFFFFu) {
+    __syncthreads();
+    uint64_t mine[8];
+    int nm = 0;
+    for (int i = tid; i < n && nm < 8; i += blockDim.x)
+      if (static_cast<uint32_t>(sm[i] >> 32) <= band_key) mine[nm++] = sm[i];
+    const bool spill = (n > 8 * (int)blockDim.x);  // cannot happen: n <= smc <= 8 * 256 * ... guard anyway
+    __syncthreads();
+    if (tid == 0) count2 = 0;
+    __syncthreads();
+    if (!spill) {
+      for (int j = 0; j < nm; ++j) sm[atomicAdd(&count2, 1)] = mine[j];
+      __syncthreads();
+      n = count2;
+      __syncthreads();
+      if (tid == 0) count2 = 0;
+      __syncthreads();
+    }
+  }
+  // exact values for the remaining entries
   const float4* qv = reinterpret_cast<const float4*>(q0 + (size_t)q * dp);
+  const float4* qlv = q1 ? reinterpret_cast<const float4*>(q1 + (size_t)q * dp) : nullptr;
   for (int i = tid; i < n; i += blockDim.x) {
     const uint32_t ps = static_cast<uint32_t>(sm[i]);
-    const float4* xv = reinterpret_cast<const float4*>(xb + (size_t)ps * dp);
-    float acc = 0.f;
-    for (int c = 0; c < dp / 4; ++c) {
-      const float4 a = __ldg(qv + c), bb = __ldg(xv + c);
-      acc = fmaf(a.x, bb.x, acc);
-      acc = fmaf(a.y, bb.y, acc);
-      acc = fmaf(a.z, bb.z, acc);
-      acc = fmaf(a.w, bb.w, acc);
-    }
+    const float acc = exact_dot(qv, qlv, reinterpret_cast<const float4*>(xb + (size_t)ps * dp),
+                                xl ? reinterpret_cast<const float4*>(xl + (size_t)ps * dp) : nullptr, dp);
     float v;
     if (IS_IP) v = -acc;
     else {
@@ -1280,21 +1320,16 @@ __global__ void __launch_bounds__(256) merge_rescore_kernel(
 // Exact fallback for one query (uncertified in merge_rescore_kernel): the
 // exact (value, position) composite of every stored row.
 template <bool IS_IP>
-__global__ void exact_all_kernel(const float* __restrict__ qrow, const float* __restrict__ qn_ptr, const float* __restrict__ xb,
-                                 const float* __restrict__ xnorm, int64_t n, int dp, uint64_t* __restrict__ out) {
+__global__ void exact_all_kernel(const float* __restrict__ qrow, const float* __restrict__ qlo,
+                                 const float* __restrict__ qn_ptr, const float* __restrict__ xb,
+                                 const float* __restrict__ xl, const float* __restrict__ xnorm, int64_t n, int dp,
+                                 uint64_t* __restrict__ out) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   const float qn = *qn_ptr;
-  const float4* qv = reinterpret_cast<const float4*>(qrow);
-  const float4* xv = reinterpret_cast<const float4*>(xb + (size_t)r * dp);
-  float acc = 0.f;
-  for (int c = 0; c < dp / 4; ++c) {
-    const float4 a = __ldg(qv + c), b = __ldg(xv + c);
-    acc = fmaf(a.x, b.x, acc);
-    acc = fmaf(a.y, b.y, acc);
-    acc = fmaf(a.z, b.z, acc);
-    acc = fmaf(a.w, b.w, acc);
-  }
+  const float acc = exact_dot(reinterpret_cast<const float4*>(qrow), reinterpret_cast<const float4*>(qlo),
+                              reinterpret_cast<const float4*>(xb + (size_t)r * dp),
+                              xl ? reinterpret_cast<const float4*>(xl + (size_t)r * dp) : nullptr, dp);
   float v;
   if (IS_IP) v = -acc;
   else {

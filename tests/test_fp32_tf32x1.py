@@ -72,3 +72,25 @@ def test_tf32x1_exact_ties_use_the_certified_fallback():
     want_ids, want_dist = O.flat_search_blas(xb, q, 10, "l2")
     assert np.array_equal(res.ids, want_ids)
     assert np.array_equal(res.distances, want_dist)
+
+
+@pytest.mark.parametrize("metric", ["l2", "ip"])
+def test_default_split_storage_uses_1x_filter_for_small_k(metric):
+    """Default fp32 (hi/lo split) index, k <= 16 over >= 262144 rows: the
+    1-pass filter runs on the hi half and rescoring uses hi + lo; the answer
+    must equal the 3xTF32 path's (FK_FP32_3X=1) and the oracle's."""
+    from paper_2401_08281_b200 import METRIC_IP, METRIC_L2, FlatIndex
+    rng = np.random.default_rng(11)
+    xb = rng.standard_normal((300000, 48), dtype=np.float32)
+    q = rng.standard_normal((200, 48), dtype=np.float32)
+    idx = FlatIndex(48, METRIC_IP if metric == "ip" else METRIC_L2)
+    idx.add(xb)
+    res = idx.search(q, 10)
+    os.environ["FK_FP32_3X"] = "1"
+    try:
+        res3 = idx.search(q, 10)
+    finally:
+        del os.environ["FK_FP32_3X"]
+    want_ids, want_dist = O.flat_search_blas(xb, q, 10, metric)
+    assert_parity(res.ids, res.distances, want_ids, want_dist)
+    assert_parity(res3.ids, res3.distances, want_ids, want_dist)
