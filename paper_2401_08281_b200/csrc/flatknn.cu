@@ -756,7 +756,10 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
   if (ev) CK(cudaEventRecord(ev[1], st));
   if ((rc = run_fused(h, pl, nq, h->ntotal, kp, ip, st))) return rc;
   if (ev) CK(cudaEventRecord(ev[2], st));
-  if ((rc = h->rfail.ensure((size_t)nq * sizeof(int)))) return rc;
+  if ((rc = h->rfail.ensure((size_t)(2 * nq + 1) * sizeof(int)))) return rc;
+  int* fcount = static_cast<int*>(h->rfail.p) + 2 * nq;  // device list of uncertified queries
+  int* flist = static_cast<int*>(h->rfail.p) + nq;
+  CK(cudaMemsetAsync(fcount, 0, sizeof(int), st));
   const int smc = std::min(MERGE_SMC, std::max(1024, 8 * kp));
   int p2 = 1;
   while (p2 < k) p2 <<= 1;
@@ -766,8 +769,6 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
                             (MERGE_SMC + FK_MAX_K) * 8));
     CK(cudaFuncSetAttribute(merge_rescore_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (MERGE_SMC + FK_MAX_K) * 8));
-    CK(cudaFuncSetAttribute(select_topk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, FK_MAX_K * 8));
-    CK(cudaFuncSetAttribute(select_topk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, FK_MAX_K * 8));
     cfg = true;
   }
   const size_t msmem = (size_t)(smc + p2) * 8;
@@ -785,41 +786,33 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
   if (ip)
     merge_rescore_kernel<true><<<(unsigned)nq, 256, msmem, st>>>(pk, pp, pc, pl.S_tot, (int)nq, kp, k, thr, q0, q1, xb, xl, qn,
                                                                   h->norms, h->xn_max, h->dp, h->ids, dD, dI, dP, smc,
-                                                                  fail);
+                                                                  fail, fcount, flist);
   else
     merge_rescore_kernel<false><<<(unsigned)nq, 256, msmem, st>>>(pk, pp, pc, pl.S_tot, (int)nq, kp, k, thr, q0, q1, xb, xl, qn,
                                                                    h->norms, h->xn_max, h->dp, h->ids, dD, dI, dP, smc,
-                                                                   fail);
+                                                                   fail, fcount, flist);
   CKL();
   h->nlaunch++;
-  std::vector<int> hf((size_t)nq);
-  CK(cudaMemcpyAsync(hf.data(), fail, (size_t)nq * sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  int64_t nfail = 0;
-  for (int64_t i = 0; i < nq; ++i) {
-    if (!hf[i]) continue;
-    ++nfail;
-    if ((rc = h->rcomp.ensure((size_t)h->ntotal * 8))) return rc;
-    auto comp = static_cast<uint64_t*>(h->rcomp.p);
-    const unsigned g = (unsigned)((h->ntotal + 255) / 256);
-    const float* qlo = q1 ? q1 + (size_t)i * h->dp : nullptr;
-    if (ip)
-      exact_all_kernel<true><<<g, 256, 0, st>>>(q0 + (size_t)i * h->dp, qlo, qn + i, xb, xl, h->norms, h->ntotal, h->dp,
-                                                comp);
-    else
-      exact_all_kernel<false><<<g, 256, 0, st>>>(q0 + (size_t)i * h->dp, qlo, qn + i, xb, xl, h->norms, h->ntotal,
-                                                 h->dp, comp);
-    CKL();
-    const size_t ssm = (size_t)p2 * 8;
-    if (ip)
-      select_topk_kernel<true><<<1, 256, ssm, st>>>(comp, h->ntotal, k, h->ids, dD + i * k, dI + i * k,
-                                                    dP ? dP + i * k : nullptr);
-    else
-      select_topk_kernel<false><<<1, 256, ssm, st>>>(comp, h->ntotal, k, h->ids, dD + i * k, dI + i * k,
-                                                     dP ? dP + i * k : nullptr);
-    CKL();
+  // uncertified queries: exact fallback on the device (no host sync)
+  // scratch of one exact composite per row per slot: <= 8 slots, <= 512 MB
+  const int nslots = (int)std::max<int64_t>(1, std::min<int64_t>({nq, 8, (512ll << 20) / (h->ntotal * 8)}));
+  if ((rc = h->rcomp.ensure((size_t)nslots * h->ntotal * 8))) return rc;
+  static bool fcfg = false;
+  if (!fcfg) {
+    CK(cudaFuncSetAttribute(fallback_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, FK_MAX_K * 8));
+    CK(cudaFuncSetAttribute(fallback_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, FK_MAX_K * 8));
+    fcfg = true;
   }
-  h->est_fallbacks += nfail;
+  auto comp = static_cast<uint64_t*>(h->rcomp.p);
+  const size_t ssm = (size_t)p2 * 8;
+  if (ip)
+    fallback_kernel<true><<<nslots, 256, ssm, st>>>(fcount, flist, q0, q1, qn, xb, xl, h->norms, h->ntotal, h->dp, k,
+                                                    h->ids, dD, dI, dP, comp);
+  else
+    fallback_kernel<false><<<nslots, 256, ssm, st>>>(fcount, flist, q0, q1, qn, xb, xl, h->norms, h->ntotal, h->dp, k,
+                                                     h->ids, dD, dI, dP, comp);
+  CKL();
+  h->nlaunch++;
   return FK_OK;
 }
 
@@ -1047,6 +1040,7 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
     h->plan[8] = pl.acc_stages;
     h->plan[9] = pl.epi;
     h->plan[10] = pl.bn;
+    h->plan[11] = pl.kmode;
   } else {
     const int kq = k <= 8 ? 8 : k <= 16 ? 16 : k <= 32 ? 32 : 0;  // 0: large-k buffers
 
@@ -1102,6 +1096,7 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
     h->plan[8] = pl.acc_stages;
     h->plan[9] = pl.epi;
     h->plan[10] = pl.bn;
+    h->plan[11] = pl.kmode;
   }
 
   if (!on_device) {

@@ -1181,13 +1181,18 @@ __global__ void __launch_bounds__(256) merge_rescore_kernel(
     const float* __restrict__ xb, const float* __restrict__ xl,
     const float* __restrict__ qnorm, const float* __restrict__ xnorm, const float* __restrict__ xn_max, int dp,
     const int64_t* __restrict__ ids, float* __restrict__ D, int64_t* __restrict__ I, int64_t* __restrict__ P, int smc,
-    int* __restrict__ fail) {
+    int* __restrict__ fail, int* __restrict__ fail_count, int* __restrict__ fail_list) {
   extern __shared__ uint64_t sm[];  // smc gathered entries, then the k winners (pow2-padded)
   __shared__ int count, count2;
   __shared__ uint32_t hist[256], sel[8];
   const int q = blockIdx.x;
   const int tid = threadIdx.x;
   if (q >= nq) return;
+  // uncertified queries are appended to fail_list for fallback_kernel (no host round trip)
+  auto mark_failed = [&]() {
+    fail[q] = 1;
+    fail_list[atomicAdd(fail_count, 1)] = q;
+  };
   const uint32_t thr = thr_key[q];
   const uint32_t* lk = pkey + (size_t)q * S * kp;
   const uint32_t* lp = ppos + (size_t)q * S * kp;
@@ -1213,7 +1218,7 @@ __global__ void __launch_bounds__(256) merge_rescore_kernel(
   __syncthreads();
   int n = count;
   if (n > smc) {  // more survivors than the buffer: exact fallback for this query
-    if (tid == 0) fail[q] = 1;
+    if (tid == 0) mark_failed();
     return;
   }
   // certification on the tf32 values
@@ -1231,7 +1236,10 @@ __global__ void __launch_bounds__(256) merge_rescore_kernel(
   } else if (thr != 0xFFFFFFFFu) {
     ok = false;  // fewer than k gathered although entries were dropped
   }
-  if (tid == 0) fail[q] = ok ? 0 : 1;
+  if (tid == 0) {
+    if (ok) fail[q] = 0;
+    else mark_failed();
+  }
   if (!ok) return;
   // keep the band only (typically k + a few): in-place compaction
   if (band_key != 0xFFFFFFFFu) {
@@ -1317,83 +1325,90 @@ __global__ void __launch_bounds__(256) merge_rescore_kernel(
   }
 }
 
-// Exact fallback for one query (uncertified in merge_rescore_kernel): the
-// exact (value, position) composite of every stored row.
+// Exact fallback, on the device: CTA b takes failed queries b, b+grid, ...;
+// exact composites of every row into its scratch slot, block radix select of
+// the k-th, bitonic sort of the winners.  Launched after every MODE 4 merge
+// (it exits at once when nothing failed), so a search never syncs the host.
 template <bool IS_IP>
-__global__ void exact_all_kernel(const float* __restrict__ qrow, const float* __restrict__ qlo,
-                                 const float* __restrict__ qn_ptr, const float* __restrict__ xb,
-                                 const float* __restrict__ xl, const float* __restrict__ xnorm, int64_t n, int dp,
-                                 uint64_t* __restrict__ out) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n) return;
-  const float qn = *qn_ptr;
-  const float acc = exact_dot(reinterpret_cast<const float4*>(qrow), reinterpret_cast<const float4*>(qlo),
-                              reinterpret_cast<const float4*>(xb + (size_t)r * dp),
-                              xl ? reinterpret_cast<const float4*>(xl + (size_t)r * dp) : nullptr, dp);
-  float v;
-  if (IS_IP) v = -acc;
-  else {
-    v = fmaf(-2.f, acc, qn + xnorm[r]);
-    v = (v <= 0.f) ? 0.f : v;
-  }
-  out[r] = (static_cast<uint64_t>(monotone(v)) << 32) | static_cast<uint32_t>(r);
-}
-
-// Exact top-k of n composites in global memory (one CTA): radix select + sort.
-template <bool IS_IP>
-__global__ void __launch_bounds__(256) select_topk_kernel(const uint64_t* __restrict__ comp, int64_t n, int k,
-                                                          const int64_t* __restrict__ ids, float* __restrict__ D,
-                                                          int64_t* __restrict__ I, int64_t* __restrict__ P) {
+__global__ void __launch_bounds__(256) fallback_kernel(const int* __restrict__ fail_count,
+                                                       const int* __restrict__ fail_list, const float* __restrict__ q0,
+                                                       const float* __restrict__ q1, const float* __restrict__ qnorm,
+                                                       const float* __restrict__ xb, const float* __restrict__ xl,
+                                                       const float* __restrict__ xnorm, int64_t n, int dp, int k,
+                                                       const int64_t* __restrict__ ids, float* __restrict__ D,
+                                                       int64_t* __restrict__ I, int64_t* __restrict__ P,
+                                                       uint64_t* __restrict__ scratch) {
   extern __shared__ uint64_t win[];
   __shared__ int count;
   __shared__ uint32_t hist[256], sel[8];
   const int tid = threadIdx.x;
-  if (tid == 0) count = 0;
-  __syncthreads();
-  const int nn = (int)n;
-  int nw;
-  if (nn <= k) {
-    for (int i = tid; i < nn; i += blockDim.x) win[i] = comp[i];
-    nw = nn;
-  } else {
-    const uint64_t kth = block_kth([&](int e) { return comp[e]; }, nn, (uint32_t)k, hist, sel);
-    for (int i = tid; i < nn; i += blockDim.x)
-      if (comp[i] <= kth) win[atomicAdd(&count, 1)] = comp[i];
-    __syncthreads();
-    nw = count;
-  }
-  int P2 = 1;
-  while (P2 < nw) P2 <<= 1;
-  for (int i = nw + tid; i < P2; i += blockDim.x) win[i] = ~0ull;
-  __syncthreads();
-  for (int size = 2; size <= P2; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = tid; i < P2 / 2; i += blockDim.x) {
-        const int lo = 2 * i - (i & (stride - 1));
-        const int hi = lo + stride;
-        const bool asc = (lo & size) == 0;
-        const uint64_t a = win[lo], b = win[hi];
-        if ((a > b) == asc) {
-          win[lo] = b;
-          win[hi] = a;
-        }
+  const int nf = *fail_count;
+  uint64_t* comp = scratch + (size_t)blockIdx.x * n;
+  for (int f = blockIdx.x; f < nf; f += gridDim.x) {
+    const int q = fail_list[f];
+    const float qn = qnorm[q];
+    const float4* qh = reinterpret_cast<const float4*>(q0 + (size_t)q * dp);
+    const float4* ql = q1 ? reinterpret_cast<const float4*>(q1 + (size_t)q * dp) : nullptr;
+    for (int64_t r = tid; r < n; r += blockDim.x) {
+      const float acc = exact_dot(qh, ql, reinterpret_cast<const float4*>(xb + (size_t)r * dp),
+                                  xl ? reinterpret_cast<const float4*>(xl + (size_t)r * dp) : nullptr, dp);
+      float v;
+      if (IS_IP) v = -acc;
+      else {
+        v = fmaf(-2.f, acc, qn + xnorm[r]);
+        v = (v <= 0.f) ? 0.f : v;
       }
-      __syncthreads();
+      comp[r] = (static_cast<uint64_t>(monotone(v)) << 32) | static_cast<uint32_t>(r);
     }
-  }
-  for (int r = tid; r < k; r += blockDim.x) {
-    const uint64_t w = r < nw ? win[r] : ~0ull;
-    if (w == ~0ull) {
-      D[r] = IS_IP ? -INFINITY : INFINITY;
-      I[r] = -1;
-      if (P) P[r] = -1;
+    if (tid == 0) count = 0;
+    __syncthreads();
+    const int nn = (int)n;
+    int nw;
+    if (nn <= k) {
+      for (int i = tid; i < nn; i += blockDim.x) win[i] = comp[i];
+      nw = nn;
     } else {
-      const uint32_t ps = static_cast<uint32_t>(w);
-      const float v = unmonotone(static_cast<uint32_t>(w >> 32));
-      D[r] = IS_IP ? -v : v;
-      I[r] = ids[ps];
-      if (P) P[r] = ps;
+      const uint64_t kth = block_kth([&](int e) { return comp[e]; }, nn, (uint32_t)k, hist, sel);
+      for (int i = tid; i < nn; i += blockDim.x)
+        if (comp[i] <= kth) win[atomicAdd(&count, 1)] = comp[i];
+      __syncthreads();
+      nw = count;
     }
+    int P2 = 1;
+    while (P2 < nw) P2 <<= 1;
+    for (int i = nw + tid; i < P2; i += blockDim.x) win[i] = ~0ull;
+    __syncthreads();
+    for (int size = 2; size <= P2; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = tid; i < P2 / 2; i += blockDim.x) {
+          const int lo = 2 * i - (i & (stride - 1));
+          const int hi = lo + stride;
+          const bool asc = (lo & size) == 0;
+          const uint64_t a = win[lo], b = win[hi];
+          if ((a > b) == asc) {
+            win[lo] = b;
+            win[hi] = a;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (int r = tid; r < k; r += blockDim.x) {
+      const size_t o = (size_t)q * k + r;
+      const uint64_t w = r < nw ? win[r] : ~0ull;
+      if (w == ~0ull) {
+        D[o] = IS_IP ? -INFINITY : INFINITY;
+        I[o] = -1;
+        if (P) P[o] = -1;
+      } else {
+        const uint32_t ps = static_cast<uint32_t>(w);
+        const float v = unmonotone(static_cast<uint32_t>(w >> 32));
+        D[o] = IS_IP ? -v : v;
+        I[o] = ids[ps];
+        if (P) P[o] = ps;
+      }
+    }
+    __syncthreads();
   }
 }
 

@@ -230,7 +230,7 @@ class FlatIndex(Index):
     def last_plan(self) -> dict:
         v = (ctypes.c_int * 12)()  # FK_PLAN_INTS
         N.check(N.lib().fk_last_plan(self._h, v))
-        keys = ("grid", "S", "chunk_tiles", "units", "stages", "a_mode", "smem", "kq", "acc_stages", "epi", "bn")
+        keys = ("grid", "S", "chunk_tiles", "units", "stages", "a_mode", "smem", "kq", "acc_stages", "epi", "bn", "kmode")
         return dict(zip(keys, list(v)))
 
 

@@ -18,7 +18,8 @@ import sys
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 tag = sys.argv[1]
 src = os.path.join(REPO, "gpurun_out")
-dst = os.path.join(REPO, "profiles", tag)
+reps = sys.argv[sys.argv.index("--reps") + 1] if "--reps" in sys.argv else src
+dst = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else os.path.join(REPO, "profiles", tag)
 os.makedirs(dst, exist_ok=True)
 
 
@@ -35,7 +36,7 @@ def to_bytes(v, unit):
 
 traffic = {}
 for rep, name in ((f"full_{tag}.ncu-rep", "cfg2"), (f"full5_{tag}.ncu-rep", "cfg5_2M")):
-    p = os.path.join(src, rep)
+    p = os.path.join(reps, rep)
     if not os.path.exists(p):
         continue
     summ = subprocess.run([sys.executable, os.path.join(REPO, "scripts", "ncu_summary.py"), p, "--source", "40"],
@@ -48,12 +49,13 @@ for rep, name in ((f"full_{tag}.ncu-rep", "cfg2"), (f"full5_{tag}.ncu-rep", "cfg
     traffic[name] = {"kernel": r["Kernel Name"], "dram_read_bytes": rd, "dram_write_bytes": wr,
                      "traffic_bytes": rd + wr, "duration_ms": float(r["gpu__time_duration.sum"].replace(",", "")),
                      "capture": f"profiles/{tag}/ncu_full_fused_{name}.txt"}
+print("summaries ->", dst)
 for f in (f"launches_{tag}.csv", f"bench_{tag}.json", f"sweep_{tag}.jsonl"):
     if os.path.exists(os.path.join(src, f)):
         shutil.copy(os.path.join(src, f), os.path.join(dst, f))
 with open(os.path.join(dst, "ncu_traffic.json"), "w") as f:
     json.dump(traffic, f, indent=1)
-if traffic:
+if traffic and "--out" not in sys.argv:
     with open(os.path.join(REPO, "profiles", "ncu_traffic.json"), "w") as f:
         json.dump(dict(traffic, tag=tag), f, indent=1)
 print(json.dumps(traffic, indent=1))
