@@ -536,7 +536,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
           __syncwarp();
           if (tr) p.trace[tcount * 16 + 3] = clock64();
         }
-        if (a_mode == 1) {
+        if (a_mode != 2) {  // the unit's MMAs retired: A may be replaced (smem: producer, TMEM: epilogue)
           if (elect_one()) mma_commit(aempty);
           __syncwarp();
         }
@@ -555,7 +555,8 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     uint32_t tcount = 0, a_buf = 0, a_ph = 0;
     uint32_t xs0 = 0, xp0 = 0, xs1 = 0, xp1 = 0;  // norm sub-ring positions (ring = tile % n_issuers)
     const uint32_t xh = (uint32_t)xn_slots / (uint32_t)p.n_issuers;
-    for (int u = ublock; u < p.num_units; u += ugrid) {
+    int uj = 0;  // units processed by this CTA
+    for (int u = ublock; u < p.num_units; u += ugrid, ++uj) {
       const int chunk = u / p.num_mu;
       const int m = (u - chunk * p.num_mu) * CL + (int)crank;
       const int t0 = chunk * p.chunk_tiles;
@@ -565,7 +566,10 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
 
       if (a_mode == 0) {
         // Query tile -> TMEM (lane = query row, columns = K; fp32: [hi | lo]).
-        // Safe: every MMA of the previous unit retired before its last tfull.
+        // Only after EVERY MMA of the previous unit retired (both issuers
+        // commit aempty at unit end): with two epilogue groups, this group's
+        // last tile is not necessarily the unit's last MMA.
+        if (uj > 0) mbar_wait(aempty, (uj - 1) & 1);
         for (int cc = h; cc < a_cols / 32; cc += NH) {
           uint32_t v[32];
           const uint32_t* src;

@@ -94,3 +94,31 @@ def test_default_split_storage_uses_1x_filter_for_small_k(metric):
     want_ids, want_dist = O.flat_search_blas(xb, q, 10, metric)
     assert_parity(res.ids, res.distances, want_ids, want_dist)
     assert_parity(res3.ids, res3.distances, want_ids, want_dist)
+
+
+@pytest.mark.parametrize("force", [("FK_EPI", "8"), ("FK_FORCE_S", "7"), ("FK_FORCE_S", "13"), ("FK_FORCE_AMODE", "1"),
+                                   ("FK_STAGES", "4"), ("FK_FP32_3X", "1")])
+def test_1x_path_plan_invariance(force):
+    """Default fp32 index over >= 262144 rows (1-pass filter + exact rescoring):
+    bit-identical answers across epilogue widths, odd/even chunk lengths,
+    operand placement, pipeline depth and the 3xTF32 path (regression: with
+    two epilogue groups the TMEM query operand of the next unit must wait for
+    every MMA of the previous unit)."""
+    import torch
+    from paper_2401_08281_b200 import METRIC_L2, FlatIndex
+    rng = np.random.default_rng(12)
+    xb = rng.standard_normal((300000, 128), dtype=np.float32)
+    q = torch.from_numpy(rng.standard_normal((3000, 128), dtype=np.float32)).cuda()
+    idx = FlatIndex(128, METRIC_L2)
+    idx.add(torch.from_numpy(xb).cuda())
+    base = idx.search(q, 10)
+    os.environ[force[0]] = force[1]
+    try:
+        alt = idx.search(q, 10)
+    finally:
+        del os.environ[force[0]]
+    if force[0] == "FK_FP32_3X":  # different arithmetic: parity, not bit equality
+        assert_parity(alt.ids.cpu().numpy(), alt.distances.cpu().numpy(), base.ids.cpu().numpy(),
+                      base.distances.cpu().numpy())
+    else:
+        assert torch.equal(base.ids, alt.ids) and torch.equal(base.distances, alt.distances)
