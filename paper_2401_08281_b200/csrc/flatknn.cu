@@ -143,10 +143,11 @@ struct fk_index {
   int64_t* ids = nullptr;    // [cap]
   DevBuf q_in, q0, q1, qn, pkey, ppos, thr, pcnt, cbuf, fail, outD, outI, outP, stage_in, stage_ids;
   // range search: candidates, exact pass, sort scratch and the CSR result
-  DevBuf rfail, rcomp;  // fp32 MODE 4: per-query certification flags, exact-fallback composites
+  DevBuf rfail, rcomp, rflag;  // fp32 MODE 4: per-query certification flags, exact-fallback composites
   DevBuf rcand, rcount, rdist, rkid, rkrd, rkeep, rrowc, rsel, rnsel, rtmp, rkid2, rkrd2, rv1, rv2, rlims, rids,
       rdist_out;
   float r_radius = 0.f;
+  int r_kfinal = 0;  // MODE 4 search: the caller's k (lists keep k' >= k)
   int64_t r_total = 0, r_nq = 0;
   unsigned long long r_cap = 0;
   long long est_fallbacks = 0;  // large-k searches whose estimated bound failed certification
@@ -667,6 +668,8 @@ int run_fused(fk_index* h, const Plan& P, int64_t nq, int64_t nb_pass, int k, bo
   sp.cluster = P.cluster;
   sp.bn = P.bn;
   sp.xbase = h->s0;
+  sp.kfinal = h->r_kfinal > 0 ? h->r_kfinal : k;
+  sp.rflag = static_cast<unsigned int*>(h->rflag.p);
   sp.radius = h->r_radius;
   sp.rcand = static_cast<unsigned long long*>(h->rcand.p);
   sp.rcount = static_cast<unsigned long long*>(h->rcount.p);
@@ -753,8 +756,13 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
   *plan_out = pl;
   if ((rc = h->thr.ensure((size_t)nq * sizeof(uint32_t)))) return rc;
   CK(cudaMemsetAsync(h->thr.p, 0xFF, (size_t)nq * sizeof(uint32_t), st));
+  if ((rc = h->rflag.ensure((size_t)nq * sizeof(unsigned int)))) return rc;
+  CK(cudaMemsetAsync(h->rflag.p, 0, (size_t)nq * sizeof(unsigned int), st));
+  h->r_kfinal = k;
   if (ev) CK(cudaEventRecord(ev[1], st));
-  if ((rc = run_fused(h, pl, nq, h->ntotal, kp, ip, st))) return rc;
+  rc = run_fused(h, pl, nq, h->ntotal, kp, ip, st);
+  h->r_kfinal = 0;
+  if (rc) return rc;
   if (ev) CK(cudaEventRecord(ev[2], st));
   if ((rc = h->rfail.ensure((size_t)(2 * nq + 1) * sizeof(int)))) return rc;
   int* fcount = static_cast<int*>(h->rfail.p) + 2 * nq;  // device list of uncertified queries
@@ -786,13 +794,21 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
   if (ip)
     merge_rescore_kernel<true><<<(unsigned)nq, 256, msmem, st>>>(pk, pp, pc, pl.S_tot, (int)nq, kp, k, thr, q0, q1, xb, xl, qn,
                                                                   h->norms, h->xn_max, h->dp, h->ids, dD, dI, dP, smc,
-                                                                  fail, fcount, flist);
+                                                                  fail, fcount, flist,
+                                                                  static_cast<const unsigned int*>(h->rflag.p));
   else
     merge_rescore_kernel<false><<<(unsigned)nq, 256, msmem, st>>>(pk, pp, pc, pl.S_tot, (int)nq, kp, k, thr, q0, q1, xb, xl, qn,
                                                                    h->norms, h->xn_max, h->dp, h->ids, dD, dI, dP, smc,
-                                                                   fail, fcount, flist);
+                                                                   fail, fcount, flist,
+                                                                  static_cast<const unsigned int*>(h->rflag.p));
   CKL();
   h->nlaunch++;
+  if (getenv("FK_DIAG")) {  // diagnostics: how many queries failed certification
+    int nf = 0;
+    CK(cudaMemcpyAsync(&nf, fcount, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    fprintf(stderr, "[fk] mode4 k=%d k'=%d nq=%lld uncertified=%d\n", k, kp, (long long)nq, nf);
+  }
   // uncertified queries: exact fallback on the device (no host sync)
   // scratch of one exact composite per row per slot: <= 8 slots, <= 512 MB
   const int nslots = (int)std::max<int64_t>(1, std::min<int64_t>({nq, 8, (512ll << 20) / (h->ntotal * 8)}));

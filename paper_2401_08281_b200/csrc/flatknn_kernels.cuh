@@ -74,6 +74,11 @@ struct SearchParams {
   int num_mu;      // query-tile units per chunk: num_m, or ceil(num_m / 2) pairs in cluster mode
   int bn;          // base rows per tile (template TBN of the launched kernel)
   const void* xbase;  // stored base rows (MODE 4: raw fp32, read for exact rescoring)
+  // MODE 4 band filter: lists keep k (= p.k) slots, the filter/publish bound
+  // is (own kfinal-th tf32 value + band); a row whose queue dropped an entry
+  // inside that band is flagged in rflag (the merge then uses the fallback)
+  int kfinal;
+  unsigned int* rflag;
   // range search (KQ == -1): every (row, position) whose fast-filter value
   // passes the conservative radius bound is appended to rcand (the exact
   // direct distance and the radius test follow in range_exact_kernel)
@@ -614,8 +619,23 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       uint32_t lkey = 0xFFFFFFFFu;  // key of the k-th after the last compaction
       uint32_t* hist = hist_base + ew * 256;
       if constexpr (KQ == 0) mybuf = p.cbuf + (((size_t)blockIdx.x * EPI + ew) * 32 + lane) * (size_t)p.cap;
+      // MODE 4: |t - v| <= e for every pair, band = 2e with 2x safety (see
+      // merge_rescore_kernel); the bound we filter and publish with is
+      // (own kfinal-th t) + band >= (global kfinal-th t) + band
+      const float band4 = (MODE == 4 && KQ > 0 && !RANGE && row_ok)
+                              ? (IS_IP ? 0.0078125f : 0.015625f) * sqrtf(fmaxf(p.qnorm[row], 0.f) * fmaxf(*p.xn_max, 0.f))
+                              : 0.f;
+      uint32_t min_lost = 0xFFFFFFFFu;  // MODE 4: smallest key dropped from a full queue
       auto own_key = [&]() -> uint32_t {
-        if constexpr (KQ > 0) return keys[KQS - 1];
+        if constexpr (KQ > 0) {
+          if (MODE == 4) {
+            const uint32_t kk = keys[(KQS - k) + p.kfinal - 1];
+            if (kk == 0xFFFFFFFFu) return kk;
+            const float b = unmonotone(kk) + band4;
+            return (b != b) ? 0xFFFFFFFFu : monotone(b);
+          }
+          return keys[KQS - 1];
+        }
         return lkey;
       };
       // Effective threshold = min(own k-th, best k-th published by any unit of
@@ -755,8 +775,13 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             if (!(v > thr)) {
               if (!IS_IP) v = (v <= 0.f) ? 0.f : v;  // np.maximum(dmat, 0) (flat.py:112)
               if constexpr (KQ > 0) {
-                queue_insert<KQS>(keys, pos, monotone(v), static_cast<uint32_t>(n0 + c0 + j));
-                thr = unmonotone(min(keys[KQS - 1], gkey));
+                const uint32_t kv = monotone(v);
+                if (MODE == 4) {  // band filter: track what a full queue drops
+                  if (kv >= keys[KQS - 1]) min_lost = min(min_lost, kv);
+                  else if (pos[KQS - 1] != 0xFFFFFFFFu) min_lost = min(min_lost, keys[KQS - 1]);
+                }
+                queue_insert<KQS>(keys, pos, kv, static_cast<uint32_t>(n0 + c0 + j));
+                thr = unmonotone(min(own_key(), gkey));
                 T = filter_bound(thr);
               } else {
                 mybuf[cnt++] = (static_cast<uint64_t>(monotone(v)) << 32) | static_cast<uint32_t>(n0 + c0 + j);
@@ -831,7 +856,14 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         // nothing per unit: candidates went straight to rcand
       } else if constexpr (KQ > 0) {
         if (row_ok) {
-          atomicMin(p.thr_key + row, keys[KQ - 1]);
+          atomicMin(p.thr_key + row, own_key());
+          if (MODE == 4 && min_lost != 0xFFFFFFFFu && min_lost <= own_key()) {
+            atomicOr(p.rflag + row, 1u);  // band member dropped
+            if (FK_DEV && row < 3)
+              printf("row %d chunk %d: min_lost %f own(kth+band) %f keys0 %f keys9 %f keys31 %f band %f gkey %f\n", row,
+                     chunk, unmonotone(min_lost), unmonotone(own_key()), unmonotone(keys[0]),
+                     unmonotone(keys[KQS - k + p.kfinal - 1]), unmonotone(keys[KQS - 1]), band4, unmonotone(gkey));
+          }
 #pragma unroll
           for (int i = 0; i < KQ; ++i) {
             if (i >= KQ - k) {
@@ -1185,7 +1217,8 @@ __global__ void __launch_bounds__(256) merge_rescore_kernel(
     const float* __restrict__ xb, const float* __restrict__ xl,
     const float* __restrict__ qnorm, const float* __restrict__ xnorm, const float* __restrict__ xn_max, int dp,
     const int64_t* __restrict__ ids, float* __restrict__ D, int64_t* __restrict__ I, int64_t* __restrict__ P, int smc,
-    int* __restrict__ fail, int* __restrict__ fail_count, int* __restrict__ fail_list) {
+    int* __restrict__ fail, int* __restrict__ fail_count, int* __restrict__ fail_list,
+    const unsigned int* __restrict__ rflag) {
   extern __shared__ uint64_t sm[];  // smc gathered entries, then the k winners (pow2-padded)
   __shared__ int count, count2;
   __shared__ uint32_t hist[256], sel[8];
@@ -1236,10 +1269,12 @@ __global__ void __launch_bounds__(256) merge_rescore_kernel(
     const float tk = unmonotone(static_cast<uint32_t>(kth >> 32));
     const float lim = tk + e2 + 9.5367431640625e-07f * (fabsf(tk) + qn);
     band_key = monotone(lim);
-    if (thr != 0xFFFFFFFFu) ok = unmonotone(thr) > lim;
   } else if (thr != 0xFFFFFFFFu) {
     ok = false;  // fewer than k gathered although entries were dropped
   }
+  // the fused pass filtered with (own k-th t + band) bounds, which never drop a
+  // band member; a row is uncertified only if a full queue dropped one
+  if (rflag[q]) ok = false;
   if (tid == 0) {
     if (ok) fail[q] = 0;
     else mark_failed();
