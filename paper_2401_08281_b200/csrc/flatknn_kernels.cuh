@@ -816,13 +816,17 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
               for (int j = 0; j < PIECE; ++j)
                 if (pc * PIECE + j < nvalid) p.dbg_ip[(size_t)row * p.nb + n0 + pc * PIECE + j] = __uint_as_float(racc[j]);
             }
-            // fast path: straight-line min tree, a single branch per piece
+            // fast path: straight-line min tree, a single branch per piece;
+            // the 32-column minima are kept so the slow path visits only the
+            // chunks that hold a candidate
             float m = 0.f;
+            float mcs[PIECE / 32];
 #pragma unroll
             for (int c = 0; c < PIECE / 32; ++c) {
               float f[32];
               chunk_f(*reinterpret_cast<const uint32_t(*)[32]>(&racc[32 * c]), pc * PIECE + c * 32, f);
               const float mc = IS_IP ? -reduce32<true>(f) : reduce32<false>(f);
+              mcs[c] = mc;
               m = (c == 0) ? mc : fmin_nan(m, mc);
             }
             const bool slow = !(m > T) && row_ok && !(FK_DEV && (p.dbg_flags & 4));
@@ -830,10 +834,19 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
               const unsigned sb = __ballot_sync(FULLMASK, slow);
               if (tr) p.trace[tcount * 16 + 8] += __popc(sb);
             }
+            if (FK_DEV && p.trace != nullptr) {  // slow-path statistics over all CTAs (trace row 256)
+              const unsigned sbl = __ballot_sync(FULLMASK, slow);
+              if (lane == 0) {
+                atomicAdd(reinterpret_cast<unsigned long long*>(p.trace + 256 * 16 + 0), 1ull);  // warp-pieces
+                if (sbl) atomicAdd(reinterpret_cast<unsigned long long*>(p.trace + 256 * 16 + 1), 1ull);
+                atomicAdd(reinterpret_cast<unsigned long long*>(p.trace + 256 * 16 + 2), (unsigned long long)__popc(sbl));
+              }
+            }
             if (slow) {  // divergent, rare
 #pragma unroll
               for (int c = 0; c < PIECE / 32; ++c)
-                slow_chunk(*reinterpret_cast<const uint32_t(*)[32]>(&racc[32 * c]), pc * PIECE + c * 32);
+                if (!(mcs[c] > T))  // (T only tightens while inserting: re-checked per chunk)
+                  slow_chunk(*reinterpret_cast<const uint32_t(*)[32]>(&racc[32 * c]), pc * PIECE + c * 32);
             }
             __syncwarp();
             // warp-uniform: make room for the next piece's candidates per row

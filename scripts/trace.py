@@ -17,11 +17,12 @@ idx = FlatIndex(cfg["d"], METRIC_L2 if cfg["metric"] == "l2" else METRIC_IP, sto
 idx.add(torch.from_numpy(gen_base(dict(cfg, nb=nb))).cuda())
 q = torch.from_numpy(gen_queries(cfg)).cuda()
 idx.search(q, cfg["k"]); torch.cuda.synchronize()
-buf = torch.zeros(256 * 16, dtype=torch.int64, device="cuda")
+buf = torch.zeros(257 * 16, dtype=torch.int64, device="cuda")
 N.check(N.lib().fk_debug_set_trace(idx._h, ctypes.c_void_p(buf.data_ptr())))
 idx.search(q, cfg["k"]); torch.cuda.synchronize()
 N.check(N.lib().fk_debug_set_trace(idx._h, None))
-t = buf.cpu().numpy().reshape(256, 16).astype(np.int64)
+t_all = buf.cpu().numpy().reshape(257, 16).astype(np.int64)
+t = t_all[:256]
 t0 = t[0, 0]
 print("plan", idx.last_plan(), os.environ.get("FK_DEBUG_FLAGS"))
 for i in list(range(100, 106)):
@@ -42,3 +43,5 @@ print("epilogue group 0: LDTM piece0 latency", m(t[ev, 11] - t[ev, 2]), "| piece
       "| piece1 compute + tail", m(t[ev, 7] - t[ev, 12]), "| got tfull -> ld issue", m(t[ev, 2] - t[ev, 6]))
 slow = t[:, 8]
 print("slow-path lanes per tile (warp 4): mean", slow[sl].mean(), "tiles with any", (slow[sl] > 0).mean())
+print("ALL CTAs: warp-pieces", t_all[256, 0], "with slow path", t_all[256, 1],
+      f"({t_all[256, 1] / max(t_all[256, 0], 1):.4f})", "slow lanes", t_all[256, 2])
