@@ -749,8 +749,9 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
                  cudaStream_t st, Plan* plan_out) {
   int rc;
   // k' >= k entries per list, the slack absorbs the tf32 band around the k-th
-  const int kp = k <= 16 ? 32 : std::min(k + std::max(64, k / 4), FK_MAX_K);
-  const int kq = kp <= 32 ? 32 : 0;
+  int kp = k <= 16 ? 32 : std::min(k + std::max(64, k / 4), FK_MAX_K);
+  if (const char* e = getenv("FK_KP")) kp = std::max(k, std::min(atoi(e), FK_MAX_K));
+  const int kq = kp <= 8 ? 8 : kp <= 16 ? 16 : kp <= 32 ? 32 : 0;
   Plan pl;
   if ((rc = make_plan(h, nq, h->ntotal, kp, kq, 0, &pl, 4))) return rc;
   *plan_out = pl;
