@@ -3,7 +3,9 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
 
 One step = one search of all nq=10k queries against the whole database
-(1M x 128 fp32, 3xTF32, L2, k=10), inputs already resident in HBM.  For N>1
+(1M x 128 fp32, L2, k=10), inputs already resident in HBM.  fp32 runs one
+TF32 tensor-core pass with certified exact rescoring for k <= 16 (3xTF32
+otherwise, or with FK_FP32_3X=1); `dtype` in the JSON line names the path.  For N>1
 (torchrun, one rank per GPU) the database rows are sharded over the ranks
 (strong scaling: fixed database, fixed nq), every rank searches its shard and
 the per-shard top-k lists are all-gathered over NCCL and merged.
@@ -37,11 +39,11 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 CONFIGS = {
-    1: dict(name="cfg1: IndexFlatL2 nb=100k d=128 nq=1k k=10 fp32 (3xTF32)", nb=100_000, d=128, nq=1_000, k=10,
+    1: dict(name="cfg1: IndexFlatL2 nb=100k d=128 nq=1k k=10 fp32", nb=100_000, d=128, nq=1_000, k=10,
             metric="l2", storage="fp32"),
-    2: dict(name="cfg2: IndexFlatL2 nb=1M d=128 nq=10k k=10 fp32 (3xTF32)", nb=1_000_000, d=128, nq=10_000, k=10,
+    2: dict(name="cfg2: IndexFlatL2 nb=1M d=128 nq=10k k=10 fp32", nb=1_000_000, d=128, nq=10_000, k=10,
             metric="l2", storage="fp32"),
-    3: dict(name="cfg3: IndexFlatL2 nb=1M d=128 nq=10k k=1024 fp32 (3xTF32)", nb=1_000_000, d=128, nq=10_000,
+    3: dict(name="cfg3: IndexFlatL2 nb=1M d=128 nq=10k k=1024 fp32", nb=1_000_000, d=128, nq=10_000,
             k=1024, metric="l2", storage="fp32"),
     4: dict(name="cfg4: IndexFlatIP nb=10M d=768 nq=10k k=100 fp16", nb=10_000_000, d=768, nq=10_000, k=100,
             metric="ip", storage="fp16"),
