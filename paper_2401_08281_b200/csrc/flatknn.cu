@@ -669,6 +669,8 @@ int run_fused(fk_index* h, const Plan& P, int64_t nq, int64_t nb_pass, int k, bo
   sp.bn = P.bn;
   sp.xbase = h->s0;
   sp.kfinal = h->r_kfinal > 0 ? h->r_kfinal : k;
+  sp.pub_mask = 15;
+  if (const char* e = getenv("FK_PUB")) sp.pub_mask = std::max(0, atoi(e));
   sp.rflag = static_cast<unsigned int*>(h->rflag.p);
   sp.radius = h->r_radius;
   sp.rcand = static_cast<unsigned long long*>(h->rcand.p);

@@ -78,6 +78,7 @@ struct SearchParams {
   // is (own kfinal-th tf32 value + band); a row whose queue dropped an entry
   // inside that band is flagged in rflag (the merge then uses the fallback)
   int kfinal;
+  int pub_mask;  // publish the own bound / fetch the shared one every pub_mask+1 own tiles
   unsigned int* rflag;
   // range search (KQ == -1): every (row, position) whose fast-filter value
   // passes the conservative radius bound is appended to rcand (the exact
@@ -856,7 +857,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         __syncwarp();
         if (tr) p.trace[tcount * 16 + 7] = clock64();
         if (lane == 0 && XN_TILE) mbar_arrive(&xempty[xslot]);
-        if (!RANGE && (++own_tiles & 15) == 0 && row_ok) {  // publish own k-th, fetch the shared bound
+        if (!RANGE && (++own_tiles & p.pub_mask) == 0 && row_ok) {  // publish own k-th, fetch the shared bound
           const uint32_t mine = own_key();
           gkey = min(atomicMin(p.thr_key + row, mine), mine);
           thr = unmonotone(min(mine, gkey));
