@@ -143,11 +143,12 @@ struct fk_index {
   int64_t* ids = nullptr;    // [cap]
   DevBuf q_in, q0, q1, qn, pkey, ppos, thr, pcnt, cbuf, fail, outD, outI, outP, stage_in, stage_ids;
   // range search: candidates, exact pass, sort scratch and the CSR result
-  DevBuf rfail, rcomp, rflag;  // fp32 MODE 4: per-query certification flags, exact-fallback composites
+  DevBuf rfail, rcomp, rflag, glock, gkeys;  // fp32 MODE 4: per-query certification flags, exact-fallback composites
   DevBuf rcand, rcount, rdist, rkid, rkrd, rkeep, rrowc, rsel, rnsel, rtmp, rkid2, rkrd2, rv1, rv2, rlims, rids,
       rdist_out;
   float r_radius = 0.f;
   int r_kfinal = 0;  // MODE 4 search: the caller's k (lists keep k' >= k)
+  bool r_union = false;  // MODE 4 search: maintain the per-query running union bound
   int64_t r_total = 0, r_nq = 0;
   unsigned long long r_cap = 0;
   long long est_fallbacks = 0;  // large-k searches whose estimated bound failed certification
@@ -672,6 +673,8 @@ int run_fused(fk_index* h, const Plan& P, int64_t nq, int64_t nb_pass, int k, bo
   sp.pub_mask = 15;
   if (const char* e = getenv("FK_PUB")) sp.pub_mask = std::max(0, atoi(e));
   sp.rflag = static_cast<unsigned int*>(h->rflag.p);
+  sp.glock = h->r_union ? static_cast<unsigned int*>(h->glock.p) : nullptr;
+  sp.gkeys = h->r_union ? static_cast<uint32_t*>(h->gkeys.p) : nullptr;
   sp.radius = h->r_radius;
   sp.rcand = static_cast<unsigned long long*>(h->rcand.p);
   sp.rcount = static_cast<unsigned long long*>(h->rcount.p);
@@ -761,10 +764,19 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
   CK(cudaMemsetAsync(h->thr.p, 0xFF, (size_t)nq * sizeof(uint32_t), st));
   if ((rc = h->rflag.ensure((size_t)nq * sizeof(unsigned int)))) return rc;
   CK(cudaMemsetAsync(h->rflag.p, 0, (size_t)nq * sizeof(unsigned int), st));
+  const bool gunion = !getenv("FK_NO_UNION");
+  if (gunion) {
+    if ((rc = h->glock.ensure((size_t)nq * sizeof(unsigned int))) || (rc = h->gkeys.ensure((size_t)nq * 32 * 4)))
+      return rc;
+    CK(cudaMemsetAsync(h->glock.p, 0, (size_t)nq * sizeof(unsigned int), st));
+    CK(cudaMemsetAsync(h->gkeys.p, 0xFF, (size_t)nq * 32 * 4, st));
+  }
+  h->r_union = gunion;
   h->r_kfinal = k;
   if (ev) CK(cudaEventRecord(ev[1], st));
   rc = run_fused(h, pl, nq, h->ntotal, kp, ip, st);
   h->r_kfinal = 0;
+  h->r_union = false;
   if (rc) return rc;
   if (ev) CK(cudaEventRecord(ev[2], st));
   if ((rc = h->rfail.ensure((size_t)(2 * nq + 1) * sizeof(int)))) return rc;

@@ -79,6 +79,10 @@ struct SearchParams {
   // inside that band is flagged in rflag (the merge then uses the fallback)
   int kfinal;
   int pub_mask;  // publish the own bound / fetch the shared one every pub_mask+1 own tiles
+  // MODE 4: per-query running union of the finished units' best k' tf32 keys
+  // (lock-protected), so the shared bound tightens towards the global k-th
+  unsigned int* glock;  // [nq]
+  uint32_t* gkeys;      // [nq][32]
   unsigned int* rflag;
   // range search (KQ == -1): every (row, position) whose fast-filter value
   // passes the conservative radius bound is appended to rcand (the exact
@@ -871,6 +875,39 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       } else if constexpr (KQ > 0) {
         if (row_ok) {
           atomicMin(p.thr_key + row, own_key());
+          if (MODE == 4 && p.gkeys != nullptr && k <= 32) {
+            // merge this unit's list into the query's running union (sorted,
+            // 32 deep) and publish (union k-th + band): a valid bound that,
+            // unlike one unit's own k-th, improves as units finish
+            uint32_t mk[KQS];
+#pragma unroll
+            for (int i = 0; i < KQS; ++i) mk[i] = keys[i];
+            unsigned int* lk = p.glock + row;
+            uint32_t* G = p.gkeys + (size_t)row * 32;
+            while (atomicCAS(lk, 0u, 1u) != 0u) __nanosleep(64);
+            __threadfence();
+            uint32_t gk[32], out[32];
+            for (int i = 0; i < 32; ++i) gk[i] = __ldcg(G + i);
+            int a = KQS - k, b = 0;
+            for (int o = 0; o < 32; ++o) {
+              const uint32_t x = a < KQS ? mk[a] : 0xFFFFFFFFu, y = b < 32 ? gk[b] : 0xFFFFFFFFu;
+              if (x <= y) {
+                out[o] = x;
+                ++a;
+              } else {
+                out[o] = y;
+                ++b;
+              }
+            }
+            for (int o = 0; o < 32; ++o) __stcg(G + o, out[o]);
+            __threadfence();
+            atomicExch(lk, 0u);
+            const uint32_t uk = out[p.kfinal - 1];
+            if (uk != 0xFFFFFFFFu) {
+              const float bnd = unmonotone(uk) + band4;
+              if (bnd == bnd) atomicMin(p.thr_key + row, monotone(bnd));
+            }
+          }
           if (MODE == 4 && min_lost != 0xFFFFFFFFu && min_lost <= own_key()) {
             atomicOr(p.rflag + row, 1u);  // band member dropped
             if (FK_DEV && row < 3)
