@@ -764,7 +764,7 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
   CK(cudaMemsetAsync(h->thr.p, 0xFF, (size_t)nq * sizeof(uint32_t), st));
   if ((rc = h->rflag.ensure((size_t)nq * sizeof(unsigned int)))) return rc;
   CK(cudaMemsetAsync(h->rflag.p, 0, (size_t)nq * sizeof(unsigned int), st));
-  const bool gunion = !getenv("FK_NO_UNION");
+  const bool gunion = pl.num_units >= 4 * pl.grid && !getenv("FK_NO_UNION");
   if (gunion) {
     if ((rc = h->glock.ensure((size_t)nq * sizeof(unsigned int))) || (rc = h->gkeys.ensure((size_t)nq * 32 * 4)))
       return rc;
@@ -1094,6 +1094,16 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
     }
     if ((rc = h->thr.ensure((size_t)nq * sizeof(uint32_t)))) return rc;
     if ((rc = h->fail.ensure(sizeof(int)))) return rc;
+    // k <= 32: per-query running union of the finished units' top-k (exact
+    // values here, so its k-th is a valid shared bound)
+    // (only when later waves of units can profit: >= 4 units per CTA)
+    h->r_union = kq > 0 && pl.num_units >= 4 * pl.grid && !getenv("FK_NO_UNION");
+    if (h->r_union) {
+      if ((rc = h->glock.ensure((size_t)nq * sizeof(unsigned int))) || (rc = h->gkeys.ensure((size_t)nq * 32 * 4)))
+        return rc;
+      CK(cudaMemsetAsync(h->glock.p, 0, (size_t)nq * sizeof(unsigned int), st));
+      CK(cudaMemsetAsync(h->gkeys.p, 0xFF, (size_t)nq * 32 * 4, st));
+    }
     for (int attempt = 0; attempt < 2; ++attempt) {
       const bool est = attempt == 0 && m_est > 0;
       CK(cudaMemsetAsync(h->thr.p, 0xFF, (size_t)nq * sizeof(uint32_t), st));
@@ -1115,6 +1125,7 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
       h->est_fallbacks += nfail > 0;
       if (nfail == 0) break;  // every query certified: exact
     }
+    h->r_union = false;
     if (ev) CK(cudaEventRecord(ev[3], st));
     h->plan[0] = pl.grid;
     h->plan[1] = pl.S;

@@ -875,7 +875,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       } else if constexpr (KQ > 0) {
         if (row_ok) {
           atomicMin(p.thr_key + row, own_key());
-          if (MODE == 4 && p.gkeys != nullptr && k <= 32) {
+          if (p.gkeys != nullptr && k <= 32) {
             // merge this unit's list into the query's running union (sorted,
             // 32 deep) and publish (union k-th + band): a valid bound that,
             // unlike one unit's own k-th, improves as units finish
