@@ -681,6 +681,9 @@ int run_fused(fk_index* h, const Plan& P, int64_t nq, int64_t nb_pass, int k, bo
   sp.rcap = h->r_cap;
   sp.num_mu = P.num_mu;
   if (const char* e = getenv("FK_DEBUG_FLAGS")) sp.dbg_flags = atoi(e);
+  // streamed base tiles are re-read by every query tile of the chunk: keep
+  // them (evict_last beats evict_first by 5-9 % on cfg2/3/5, FK_B_POLICY)
+  sp.b_policy = 2;
   if (const char* e = getenv("FK_B_POLICY")) sp.b_policy = atoi(e);
   rc = launch_fused(P.epi, P.kmode, h->fold != 0, ip, P.kq, ta0, ta1, tb0, tb1, sp, P.grid, P.smem, st);
   if (rc == FK_OK) h->nlaunch++;

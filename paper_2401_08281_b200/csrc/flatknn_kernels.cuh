@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     if (lane == 0) {
       const uint32_t myring = (warp == 0) ? 0u : 1u;
       const uint64_t pol_a = policy_evict_last();
-      // streamed base: evict_first by default (FK_B_POLICY=1 normal, 2 last)
+      // streamed base: evict_last by default (FK_B_POLICY=0 first, 1 normal)
       const uint64_t pol_b = p.b_policy == 2 ? policy_evict_last()
                              : p.b_policy == 1 ? policy_evict_normal() : policy_evict_first();
       // one FIFO sub-ring of `sh` slots per MMA issuer (tile t -> ring t % nis)
