@@ -1152,18 +1152,30 @@ __global__ void __launch_bounds__(256) merge_large_kernel(const uint32_t* __rest
     if (key > thr || lp[e] == 0xFFFFFFFFu) return ~0ull;
     return (static_cast<uint64_t>(key) << 32) | lp[e];
   };
-  for (int e = tid; e < total; e += blockDim.x) {  // the query's S*k block is contiguous: flat, coalesced
-    const uint32_t key = lk[e];
-    if (key > thr) continue;
-    const uint32_t ps = lp[e];
-    if (ps == 0xFFFFFFFFu) continue;
+  // the query's S*k block is contiguous: flat, coalesced, 4 independent key
+  // loads in flight per thread (the gather is latency-bound otherwise)
+  auto take = [&](int e, uint32_t key) {
+    if (key > thr) return;
+    const uint32_t ps = __ldcs(lp + e);
+    if (ps == 0xFFFFFFFFu) return;
     if (lc) {
       const int s = e / k;
-      if (e - s * k >= lc[s]) continue;
+      if (e - s * k >= lc[s]) return;
     }
     const int idx = atomicAdd(&count, 1);
     if (idx < smc) sm[idx] = (static_cast<uint64_t>(key) << 32) | ps;
+  };
+  const int step = blockDim.x;
+  int e = tid;
+  for (; e + 3 * step < total; e += 4 * step) {
+    const uint32_t k0 = __ldcs(lk + e), k1 = __ldcs(lk + e + step), k2 = __ldcs(lk + e + 2 * step),
+                   k3 = __ldcs(lk + e + 3 * step);
+    take(e, k0);
+    take(e + step, k1);
+    take(e + 2 * step, k2);
+    take(e + 3 * step, k3);
   }
+  for (; e < total; e += step) take(e, __ldcs(lk + e));
   __syncthreads();
   const int n = count;
   // certification (estimated bound): fewer than k survivors means the bound
