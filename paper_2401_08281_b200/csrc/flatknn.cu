@@ -524,6 +524,7 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   //  * otherwise A in smem, or streamed with every stage (a_mode 2).
   P.bn = 128;
   if (h->storage != FK_F32 && P.nh == 2 && a_bytes <= 64 * 1024) P.a_mode = 1;
+  else if (kmode == 4 && a_bytes <= 64 * 1024) P.a_mode = 1;  // 1-pass fp32: 4 accumulators (+2.5 %)
   else if (a_tmem_cols <= 256) P.a_mode = 0;
   else if (a_tmem_cols <= 384) {
     P.a_mode = 0;
