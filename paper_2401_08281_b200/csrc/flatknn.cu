@@ -549,6 +549,8 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   P.cluster = 1;
   if (const char* e = getenv("FK_CLUSTER")) P.cluster = atoi(e) == 2 ? 2 : 1;
   if (P.num_m < 2 || h->num_sms < 2) P.cluster = 1;
+  // (the 1-pass fp32 search certifies far fewer queries in pair mode: not used)
+  if (kmode == 4) P.cluster = 1;
   P.num_mu = (P.num_m + P.cluster - 1) / P.cluster;
   // chunk <= L2_CHUNK_BYTES of streamed base; partial lists <= PARTIAL_BYTES
   const size_t tile_bytes = (size_t)bn * h->dp * elem_bytes_of(h->storage) * split;
