@@ -1332,11 +1332,15 @@ __global__ void __launch_bounds__(256) merge_rescore_kernel(
     const float tk = unmonotone(static_cast<uint32_t>(kth >> 32));
     const float lim = tk + e2 + 9.5367431640625e-07f * (fabsf(tk) + qn);
     band_key = monotone(lim);
+    // large-k lists (pcnt != NULL) were filtered by the units' k'-th values:
+    // every entry that did not reach a list has t >= thr, so thr must clear
+    // the band.  (Register-queue lists filter with (own k-th + band) bounds,
+    // which never drop a band member: only the row flag below matters.)
+    if (lc != nullptr && thr != 0xFFFFFFFFu) ok = unmonotone(thr) > lim;
   } else if (thr != 0xFFFFFFFFu) {
     ok = false;  // fewer than k gathered although entries were dropped
   }
-  // the fused pass filtered with (own k-th t + band) bounds, which never drop a
-  // band member; a row is uncertified only if a full queue dropped one
+  // a register queue that dropped a band member flagged its row
   if (rflag[q]) ok = false;
   if (tid == 0) {
     if (ok) fail[q] = 0;
