@@ -122,3 +122,20 @@ def test_1x_path_plan_invariance(force):
                       base.distances.cpu().numpy())
     else:
         assert torch.equal(base.ids, alt.ids) and torch.equal(base.distances, alt.distances)
+
+
+@pytest.mark.parametrize("k", [10, 50])
+def test_raw_storage_exact_ties_all_k(k):
+    """Raw-fp32 storage (FK_FP32_ALGO=1): massive exact ties around the k-th
+    for both list kinds (register queue k <= 16, candidate buffers k > 16);
+    uncertified rows must go through the exact fallback and match the
+    reference order exactly."""
+    rng = np.random.default_rng(33 + k)
+    xb = rng.integers(0, 3, size=(300000, 16)).astype(np.float32)
+    q = rng.integers(0, 3, size=(40, 16)).astype(np.float32)
+    idx = _index(16, "l2")
+    idx.add(xb)
+    res = idx.search(q, k)
+    want_ids, want_dist = O.flat_search_blas(xb, q, k, "l2")
+    assert np.array_equal(res.ids, want_ids)
+    assert np.array_equal(res.distances, want_dist)
