@@ -143,7 +143,8 @@ struct fk_index {
   int64_t* ids = nullptr;    // [cap]
   DevBuf q_in, q0, q1, qn, pkey, ppos, thr, pcnt, cbuf, fail, outD, outI, outP, stage_in, stage_ids;
   // range search: candidates, exact pass, sort scratch and the CSR result
-  DevBuf rfail, rcomp, rflag, glock, gkeys;  // fp32 MODE 4: per-query certification flags, exact-fallback composites
+  DevBuf rfail, rcomp, rflag, glock, gkeys;
+  unsigned int* inexact = nullptr;  // device {base, queries}: a value with a nonzero lo part was stored/staged  // fp32 MODE 4: per-query certification flags, exact-fallback composites
   DevBuf rcand, rcount, rdist, rkid, rkrd, rkeep, rrowc, rsel, rnsel, rtmp, rkid2, rkrd2, rv1, rv2, rlims, rids,
       rdist_out;
   float r_radius = 0.f;
@@ -228,12 +229,12 @@ int kmode_of(const fk_index* h) {
 }
 
 int launch_prep(int kmode, const void* x, int dtype, int64_t n, int d, int dp, void* o0, void* o1, float* norms,
-                int64_t row0, cudaStream_t st, int fold = 0) {
+                int64_t row0, cudaStream_t st, int fold = 0, unsigned int* inexact = nullptr) {
   if (n <= 0) return FK_OK;
   const int wpb = 8;
   const unsigned grid = (unsigned)((n + wpb - 1) / wpb);
   if (kmode == 0)
-    prep_rows_kernel<0><<<grid, wpb * 32, 0, st>>>(x, dtype, n, d, dp, o0, o1, norms, row0, 0);
+    prep_rows_kernel<0><<<grid, wpb * 32, 0, st>>>(x, dtype, n, d, dp, o0, o1, norms, row0, 0, inexact);
   else if (kmode == 4)
     prep_rows_kernel<4><<<grid, wpb * 32, 0, st>>>(x, dtype, n, d, dp, o0, o1, norms, row0, 0);
   else if (kmode == 1)
@@ -404,7 +405,9 @@ int fk_create(int device, int d, int metric, int storage, fk_index** out) {
   }
   if (const char* e = getenv("FK_NO_FOLD"); e && atoi(e)) h->fold = 0;
   h->num_sms = prop.multiProcessorCount;
-  if (cudaMalloc((void**)&h->xn_max, sizeof(float)) != cudaSuccess || cudaMemset(h->xn_max, 0, sizeof(float)) != cudaSuccess) {
+  if (cudaMalloc((void**)&h->inexact, 2 * sizeof(unsigned int)) != cudaSuccess ||
+      cudaMemset(h->inexact, 0, 2 * sizeof(unsigned int)) != cudaSuccess ||
+      cudaMalloc((void**)&h->xn_max, sizeof(float)) != cudaSuccess || cudaMemset(h->xn_max, 0, sizeof(float)) != cudaSuccess) {
     delete h;
     return set_err(FK_E_NOMEM, "cudaMalloc failed");
   }
@@ -425,6 +428,7 @@ void fk_destroy(fk_index* h) {
                     &h->stage_in, &h->stage_ids})
     b->release();
   cudaFree(h->xn_max);
+  cudaFree(h->inexact);
   for (auto& q : h->ev_pool)
     for (auto& e : q) cudaEventDestroy(e);
   delete h;
@@ -438,6 +442,7 @@ int fk_reset(fk_index* h) {
   std::lock_guard<std::mutex> g(h->mu);
   CK(cudaSetDevice(h->device));
   CK(cudaMemset(h->xn_max, 0, sizeof(float)));
+  CK(cudaMemset(h->inexact, 0, 2 * sizeof(unsigned int)));
   h->ntotal = 0;
   return FK_OK;
 }
@@ -468,7 +473,7 @@ int fk_add(fk_index* h, const void* x, int64_t n, int dtype, const int64_t* ids,
       src = h->stage_in.p;
     }
     if ((rc = launch_prep(kmode_of(h), src, dtype, m, h->d, h->dp, h->s0, h->s1, h->norms, h->ntotal + r0, st,
-                          h->fold ? 1 : 0)))
+                          h->fold ? 1 : 0, h->inexact)))
       return rc;
     if (!on_device) CK(cudaStreamSynchronize(st));  // stage buffer reused by the next slice
   }
@@ -676,6 +681,7 @@ int run_fused(fk_index* h, const Plan& P, int64_t nq, int64_t nb_pass, int k, bo
   sp.pub_mask = 15;
   if (const char* e = getenv("FK_PUB")) sp.pub_mask = std::max(0, atoi(e));
   sp.rflag = static_cast<unsigned int*>(h->rflag.p);
+  sp.inexact = h->split == 2 ? h->inexact : nullptr;  // raw storage: no lo parts known -> full band
   sp.glock = h->r_union ? static_cast<unsigned int*>(h->glock.p) : nullptr;
   sp.gkeys = h->r_union ? static_cast<uint32_t*>(h->gkeys.p) : nullptr;
   sp.radius = h->r_radius;
@@ -749,8 +755,9 @@ int stage_queries(fk_index* h, const void* q, int64_t nq, int dtype, int on_devi
   if ((rc = h->q0.ensure(nq * qrow))) return rc;
   if (h->split == 2 && (rc = h->q1.ensure(nq * qrow))) return rc;
   if ((rc = h->qn.ensure(nq * sizeof(float)))) return rc;
+  if (h->inexact) CK(cudaMemsetAsync(h->inexact + 1, 0, sizeof(unsigned int), st));
   return launch_prep(kmode_of(h), qsrc, dtype, nq, h->d, h->dp, h->q0.p, h->q1.p, static_cast<float*>(h->qn.p), 0, st,
-                     h->fold ? 2 : 0);
+                     h->fold ? 2 : 0, h->inexact ? h->inexact + 1 : nullptr);
 }
 
 // fp32 MODE 4 search: fused pass with a 1-pass TF32 GEMM keeping k' >= k
@@ -816,12 +823,14 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
     merge_rescore_kernel<true><<<(unsigned)nq, 256, msmem, st>>>(pk, pp, pc, pl.S_tot, (int)nq, kp, k, thr, q0, q1, xb, xl, qn,
                                                                   h->norms, h->xn_max, h->dp, h->ids, dD, dI, dP, smc,
                                                                   fail, fcount, flist,
-                                                                  static_cast<const unsigned int*>(h->rflag.p));
+                                                                  static_cast<const unsigned int*>(h->rflag.p),
+                                                                  h->split == 2 ? h->inexact : nullptr);
   else
     merge_rescore_kernel<false><<<(unsigned)nq, 256, msmem, st>>>(pk, pp, pc, pl.S_tot, (int)nq, kp, k, thr, q0, q1, xb, xl, qn,
                                                                    h->norms, h->xn_max, h->dp, h->ids, dD, dI, dP, smc,
                                                                    fail, fcount, flist,
-                                                                  static_cast<const unsigned int*>(h->rflag.p));
+                                                                  static_cast<const unsigned int*>(h->rflag.p),
+                                                                  h->split == 2 ? h->inexact : nullptr);
   CKL();
   h->nlaunch++;
   if (getenv("FK_DIAG")) {  // diagnostics: how many queries failed certification

@@ -78,6 +78,9 @@ struct SearchParams {
   // is (own kfinal-th tf32 value + band); a row whose queue dropped an entry
   // inside that band is flagged in rflag (the merge then uses the fallback)
   int kfinal;
+  // {base, queries}: nonzero when some value needs its lo part; when both
+  // are zero the 1-pass tf32 products are exact and the band collapses
+  const unsigned int* inexact;
   int pub_mask;  // publish the own bound / fetch the shared one every pub_mask+1 own tiles
   // MODE 4: per-query running union of the finished units' best k' tf32 keys
   // (lock-protected), so the shared bound tightens towards the global k-th
@@ -627,8 +630,13 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       // MODE 4: |t - v| <= e for every pair, band = 2e with 2x safety (see
       // merge_rescore_kernel); the bound we filter and publish with is
       // (own kfinal-th t) + band >= (global kfinal-th t) + band
+      const bool tf32_exact = p.inexact != nullptr && (p.inexact[0] | p.inexact[1]) == 0u;
       const float band4 = (MODE == 4 && KQ > 0 && !RANGE && row_ok)
-                              ? (IS_IP ? 0.0078125f : 0.015625f) * sqrtf(fmaxf(p.qnorm[row], 0.f) * fmaxf(*p.xn_max, 0.f))
+                              ? (tf32_exact ? 0.f : (IS_IP ? 0.0078125f : 0.015625f)) *
+                                        sqrtf(fmaxf(p.qnorm[row], 0.f) * fmaxf(*p.xn_max, 0.f)) +
+                                    // exact products: only the two fp32 accumulation orders differ
+                                    (float)dp * 1.1920928955078125e-07f *
+                                        (fmaxf(p.qnorm[row], 0.f) + fmaxf(*p.xn_max, 0.f))
                               : 0.f;
       uint32_t min_lost = 0xFFFFFFFFu;  // MODE 4: smallest key dropped from a full queue
       auto own_key = [&]() -> uint32_t {
@@ -1281,7 +1289,7 @@ __global__ void __launch_bounds__(256) merge_rescore_kernel(
     const float* __restrict__ qnorm, const float* __restrict__ xnorm, const float* __restrict__ xn_max, int dp,
     const int64_t* __restrict__ ids, float* __restrict__ D, int64_t* __restrict__ I, int64_t* __restrict__ P, int smc,
     int* __restrict__ fail, int* __restrict__ fail_count, int* __restrict__ fail_list,
-    const unsigned int* __restrict__ rflag) {
+    const unsigned int* __restrict__ rflag, const unsigned int* __restrict__ inexact) {
   extern __shared__ uint64_t sm[];  // smc gathered entries, then the k winners (pow2-padded)
   __shared__ int count, count2;
   __shared__ uint32_t hist[256], sel[8];
@@ -1324,7 +1332,9 @@ __global__ void __launch_bounds__(256) merge_rescore_kernel(
   // certification on the tf32 values
   const float qn = qnorm[q];
   // band 2e with a 2x safety factor: L2 2 * 2 * 2^-8, IP 2 * 2 * 2^-9 (|q| max|x|)
-  const float e2 = (IS_IP ? 0.0078125f : 0.015625f) * sqrtf(fmaxf(qn, 0.f) * fmaxf(*xn_max, 0.f));
+  const bool tf32_exact = inexact != nullptr && (inexact[0] | inexact[1]) == 0u;
+  const float e2 = (tf32_exact ? 0.f : (IS_IP ? 0.0078125f : 0.015625f)) * sqrtf(fmaxf(qn, 0.f) * fmaxf(*xn_max, 0.f)) +
+                   (float)dp * 1.1920928955078125e-07f * (fmaxf(qn, 0.f) + fmaxf(*xn_max, 0.f));
   bool ok = true;
   uint32_t band_key = 0xFFFFFFFFu;  // only entries with t <= t_k + band can be in the exact top-k
   if (n >= k) {
@@ -1539,7 +1549,7 @@ __device__ __forceinline__ float tf32_rna(float v) {
 template <int MODE>
 __global__ void prep_rows_kernel(const void* __restrict__ x, int in_dtype, int64_t n, int d, int dp,
                                  void* __restrict__ out0, void* __restrict__ out1, float* __restrict__ norms,
-                                 int64_t row0, int fold) {
+                                 int64_t row0, int fold, unsigned int* __restrict__ inexact = nullptr) {
   const int64_t rloc = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (rloc >= n) return;
@@ -1550,6 +1560,7 @@ __global__ void prep_rows_kernel(const void* __restrict__ x, int in_dtype, int64
     if (MODE == 0) {
       const float hi = tf32_rna(v);
       const float lo = v - hi;  // exact: x == hi + lo
+      if (inexact != nullptr && lo != 0.f) *inexact = 1u;  // the value needs more than one tf32 term
       static_cast<float*>(out0)[(size_t)orow * dp + c] = hi;
       static_cast<float*>(out1)[(size_t)orow * dp + c] = lo;
       acc += (double)v * (double)v;

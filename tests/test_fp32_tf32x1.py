@@ -139,3 +139,29 @@ def test_raw_storage_exact_ties_all_k(k):
     want_ids, want_dist = O.flat_search_blas(xb, q, k, "l2")
     assert np.array_equal(res.ids, want_ids)
     assert np.array_equal(res.distances, want_dist)
+
+
+def test_tf32_exact_data_needs_no_fallback():
+    """SIFT-like integer data is exactly representable in tf32 (every lo part
+    is zero, detected at add/stage time): the band collapses to the fp32
+    accumulation slack, so queries certify without the exact fallback."""
+    import subprocess
+    code = r'''
+import os, sys, numpy as np
+sys.path.insert(0, os.getcwd()); sys.path.insert(0, "tests")
+from paper_2401_08281_b200 import FlatIndex, METRIC_L2
+from oracle import flat_oracle as O
+from parity import assert_parity
+rng = np.random.default_rng(8)
+xb = rng.integers(0, 256, size=(300000, 128)).astype(np.float32)
+q = rng.integers(0, 256, size=(500, 128)).astype(np.float32)
+idx = FlatIndex(128, METRIC_L2); idx.add(xb)
+res = idx.search(q, 10)
+wi, wd = O.flat_search_blas(xb, q, 10, "l2")
+assert np.array_equal(res.ids, wi) and np.array_equal(res.distances, wd)
+'''
+    env = dict(os.environ, FK_DIAG="1")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       cwd=os.path.dirname(HERE))
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "uncertified=0" in r.stderr, r.stderr[-2000:]
