@@ -106,71 +106,86 @@ def gen_queries(cfg):
     return np.random.default_rng(1).standard_normal((cfg["nq"], cfg["d"]), dtype=np.float32)
 
 
+_NVML_POLLER = r"""
+import sys, time
+import pynvml
+pynvml.nvmlInit()
+bus, idx = sys.argv[1], int(sys.argv[2])
+try:
+    h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+except Exception:
+    h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+while True:
+    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+    try:
+        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+    except AttributeError:
+        rs = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+    print(f"{sm},{mx},{rs}", flush=True)
+    time.sleep(0.02)
+"""
+
+
 class ClockSampler:
     """SM clocks / throttle reasons sampled during the timed region.
 
-    In-process NVML (nvidia_ml_py) every 50 ms: spawning nvidia-smi inside a
-    short timed region stalls GPU submission while it initialises, so it is
-    only the fallback."""
+    NVML is polled every 20 ms from a CHILD process started before warm-up
+    (an in-process poller thread, or event creation next to it, stalled the
+    timed loop's submissions in round 1); each sample is stamped on arrival
+    and `summary(t0, t1)` keeps the samples of the timed window.  nvidia-smi
+    (also a child process) is the fallback."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-    # nvmlClocksEventReason bits
     REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
 
-    def __init__(self, gpu_index):
+    def __init__(self, gpu_index, bus_id=""):
         self.gpu = gpu_index
+        self.bus = bus_id
         self.proc = None
-        self.lines = []
-        self.samples = []  # (sm_mhz, max_mhz, reasons bitmask)
-        self.stop = threading.Event()
-        self.nvml = None
+        self.samples = []  # (t_arrival, sm_mhz, max_mhz, reasons bitmask)
+        self.kind = None
 
     def __enter__(self):
-        try:
-            import pynvml
-            pynvml.nvmlInit()
-            self.nvml = pynvml
-            self.handle = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM)
-            self.t = threading.Thread(target=self._poll, daemon=True)
-            self.t.start()
-            return self
-        except Exception:
-            self.nvml = None
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except Exception:
-            self.proc = None
-        return self
-
-    def _poll(self):
-        P = self.nvml
-        while not self.stop.is_set():
+        cmds = [("nvml", [sys.executable, "-c", _NVML_POLLER, self.bus, str(self.gpu)]),
+                ("nvidia-smi", ["nvidia-smi", "-i", str(self.gpu),
+                                "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                                "--format=csv,noheader,nounits", "-lms", "20"])]
+        for kind, cmd in cmds:
             try:
-                sm = P.nvmlDeviceGetClockInfo(self.handle, P.NVML_CLOCK_SM)
-                try:
-                    rs = P.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
-                except AttributeError:
-                    rs = P.nvmlDeviceGetCurrentClocksThrottleReasons(self.handle)
-                self.samples.append((float(sm), float(self.max_mhz), int(rs)))
+                self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self.kind = kind
+                self.t = threading.Thread(target=self._read, daemon=True)
+                self.t.start()
+                break
             except Exception:
-                pass
-            self.stop.wait(0.05)
+                self.proc = None
+        # wait (bounded) for the first sample so the window is covered
+        t_end = time.time() + 20
+        while self.proc is not None and not self.samples and time.time() < t_end and self.proc.poll() is None:
+            time.sleep(0.05)
+        if self.kind == "nvml" and not self.samples:  # pynvml unusable: fall back to nvidia-smi
+            self.__exit__()
+            self.proc, self.kind = None, None
+            try:
+                self.proc = subprocess.Popen(cmds[1][1], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self.kind = "nvidia-smi"
+                self.t = threading.Thread(target=self._read, daemon=True)
+                self.t.start()
+            except Exception:
+                self.proc = None
+        return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            parts = [p.strip() for p in line.split(",")]
+            try:
+                rs = parts[2]
+                rs = int(rs, 16) if rs.startswith("0x") else int(rs)
+                self.samples.append((time.time(), float(parts[0]), float(parts[1]), rs))
+            except (ValueError, IndexError):
+                continue
 
     def __exit__(self, *a):
-        self.stop.set()
-        if self.nvml is not None:
-            self.t.join(timeout=2)
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -178,31 +193,20 @@ class ClockSampler:
             except Exception:
                 self.proc.kill()
 
-    def summary(self):
-        sm, mx, reasons = [], [], set()
-        for a, b, rs in self.samples:
-            sm.append(a)
-            mx.append(b)
+    def summary(self, t0=None, t1=None):
+        win = [s for s in self.samples if t0 is None or (t0 <= s[0] <= t1)]
+        if not win and self.samples and t0 is not None:  # window shorter than the period: nearest samples
+            mid = 0.5 * (t0 + t1)
+            win = sorted(self.samples, key=lambda s: abs(s[0] - mid))[:3]
+        if not win:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        reasons = set()
+        for _, _, _, rs in win:
             for bit, nm in self.REASONS.items():
                 if rs & bit:
                     reasons.add(nm)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                mx.append(float(parts[2]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[5:9]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm), "source": "nvml" if self.samples else "nvidia-smi"}
+        return {"sm_mhz": statistics.median(s[1] for s in win), "sm_max_mhz": max(s[2] for s in win),
+                "reasons": sorted(reasons), "samples": len(win), "source": self.kind + " (child process)"}
 
 
 def cpu_oracle_qps(xb, q, k, metric, nq_sample):
@@ -309,26 +313,32 @@ def run_ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    clk = ClockSampler(local).__enter__()  # sampling starts before warm-up: covers the whole timed region
+    props = torch.cuda.get_device_properties(local)
+    bus = "%08X:%02X:%02X.0" % (getattr(props, "pci_domain_id", 0), getattr(props, "pci_bus_id", 0),
+                                getattr(props, "pci_device_id", 0))
+    clk = ClockSampler(local, bus).__enter__()  # child process, started before warm-up
     for _ in range(args.warmup):
         index.search(q_dev, k)
     torch.cuda.synchronize()
 
-    # ---- timed region: device-resident inputs
-    local_index.set_profiling(True)
+    # ---- timed region: device-resident inputs.  Kernel-level CUDA events of
+    # every search (created up front) give the per-kernel split; one event per
+    # step boundary gives the per-step times.
+    local_index.set_profiling(True, reserve=args.steps + 8)
     local_index.kernel_times()  # reset accumulators
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     barrier()
     torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if True:
-        ev0.record(stream)
-        for _ in range(args.steps):
-            res = index.search(q_dev, k)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-    clk.__exit__()
+    t_wall0 = time.time()
+    step_ev[0].record(stream)
+    for i in range(args.steps):
+        res = index.search(q_dev, k)
+        step_ev[i + 1].record(stream)
+    torch.cuda.synchronize()
+    t_wall1 = time.time()
     barrier()
-    ms_local = ev0.elapsed_time(ev1) / args.steps
+    step_ms = [step_ev[i].elapsed_time(step_ev[i + 1]) for i in range(args.steps)]
+    ms_local = step_ev[0].elapsed_time(step_ev[-1]) / args.steps
     ms = maxr(ms_local)
     (t_prep, t_fused, t_merge), launches = local_index.kernel_times()
     local_index.set_profiling(False)
@@ -346,6 +356,7 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     e2e_ms = maxr((time.perf_counter() - t0) * 1e3 / args.steps)
     assert isinstance(r.ids, np.ndarray)
+    clk.__exit__()
 
     peaks, peaks_kind = load_peaks()
     # DRAM bytes per fused launch from the committed ncu --set full capture
@@ -399,7 +410,10 @@ def run_ours(args, cfg):
         "e2e": {"value": nq / (e2e_ms / 1e3), "unit": "queries/s", "h2d_bytes_per_step": int(q_np.nbytes),
                 "d2h_bytes_per_step": int(nq * k * (4 + 8)), "ms_per_step": e2e_ms},
         "gpu_launches": int(launches),
-        "clocks": clk.summary(),
+        "ms_per_step_median": maxr(statistics.median(step_ms)),
+        "ms_per_step_min": maxr(min(step_ms)),
+        "kernel_sum_ms": t_prep + t_fused + t_merge,
+        "clocks": clk.summary(t_wall0, t_wall1),
     }
     if world > 1:
         line["gpu_launches_note"] = "per rank; plus NCCL all-gather kernels"
@@ -419,6 +433,45 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def relaunch_ranks(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: start N ranks (one per GPU) with
+    torch.distributed.run on 127.0.0.1 and return their exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def run_dry(args, cfg):
+    """--dry-run: the N-rank plumbing without a GPU (gloo): every rank reports
+    its rank and shard of the configured database; rank 0 prints the line."""
+    import torch
+    import torch.distributed as dist
+    from paper_2401_08281_b200.sharded import shard_range
+    world, rank, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    lo, hi = shard_range(cfg["nb"], rank, world)
+    t = torch.tensor([rank, world, lo, hi], dtype=torch.int64)
+    parts = [torch.zeros_like(t) for _ in range(world)]
+    if world > 1:
+        dist.all_gather(parts, t)
+    else:
+        parts = [t]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "gpus_requested": args.gpus,
+                          "ranks": [p.tolist() for p in parts], "config": {"workload": cfg["name"]}}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -427,11 +480,19 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help="rank plumbing only (gloo, no GPU)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     cfg = CONFIGS[args.config]
-    if args.impl == "reference":
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_ranks(args.gpus))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: one rank per GPU expected")
+    if args.dry_run:
+        run_dry(args, cfg)
+    elif args.impl == "reference":
         run_reference(args, cfg)
     else:
         run_ours(args, cfg)

@@ -105,8 +105,9 @@ void fk_destroy(fk_index* h);
 
 const char* fk_last_error(void);
 
-/* Instrumentation: when enabled, fk_search records CUDA events around each of
- * its kernels on the launch stream (no host synchronisation).  fk_kernel_times
+/* Instrumentation: when enabled (on > 0; the events of `on` searches, at
+ * least 64, are created here, up front), fk_search records CUDA events around
+ * each of its kernels on the launch stream (no host synchronisation).  fk_kernel_times
  * waits for them and returns the mean durations (ms) per search since its
  * previous call: [0] query prep, [1] fused GEMM+top-k, [2] merge; *nlaunch =
  * total kernel launches of those searches.  Then it resets the accumulators. */

@@ -23,8 +23,11 @@ LIB_PATH = os.path.join(PKG_DIR, LIB_NAME)
 # loaded instead of the product library only when FK_DEV_LIB=1 (scripts/)
 DEV_LIB_PATH = os.path.join(PKG_DIR, "libflatknn_dev.so")
 
-SOURCES = ["flatknn.cu"]
-DEPS = SOURCES + ["flatknn_kernels.cuh", "sm100.cuh"]
+# one translation unit per fused-kernel operand MODE (the template
+# instantiations dominate compile time) + the host/ABI unit; compiled in
+# parallel, linked into one shared library
+SOURCES = ["flatknn.cu"] + [f"fused_m{m}.cu" for m in range(5)]
+DEPS = SOURCES + ["flatknn_kernels.cuh", "fused_kernel.cuh", "fused_launch.cuh", "fk_host.cuh", "sm100.cuh"]
 
 
 def nvcc_path() -> str:
@@ -46,23 +49,39 @@ def build(force: bool = False, verbose: bool = True, dev: bool = False) -> str:
     out = DEV_LIB_PATH if dev else LIB_PATH
     if not force and not needs_build(out):
         return out
-    cmd = [
-        nvcc_path(),
+    nvcc = nvcc_path()
+    common = [
         "-gencode", "arch=compute_100a,code=sm_100a",
         "-O3", "-lineinfo", "-std=c++17",
-        "-Xcompiler", "-fPIC,-O3", "-shared", "-cudart", "static",
+        "-Xcompiler", "-fPIC,-O3",
         "-Xptxas", "-v",
         "-I", os.path.join(REPO, "include"),
-        "-o", out + ".tmp",
-    ] + (["-DFK_DEV=1"] if dev else []) + [os.path.join(CSRC, s) for s in SOURCES]
-    if verbose:
-        print("[build]", " ".join(cmd), file=sys.stderr)
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    ] + (["-DFK_DEV=1"] if dev else [])
+    objdir = os.path.join(PKG_DIR, "_obj_dev" if dev else "_obj")
+    os.makedirs(objdir, exist_ok=True)
+    procs = []
+    for src in SOURCES:
+        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        cmd = [nvcc, "-c"] + common + ["-o", obj, os.path.join(CSRC, src)]
+        if verbose:
+            print("[build]", " ".join(cmd), file=sys.stderr)
+        procs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
+    logs, failed = [], []
+    for src, obj, pr in procs:
+        text = pr.communicate()[0]
+        logs.append(f"==== {src}\n{text}")
+        if pr.returncode != 0:
+            failed.append(src)
     log_path = os.path.join(PKG_DIR, "build_dev.log" if dev else "build.log")
     with open(log_path, "w") as f:
-        f.write(res.stdout + res.stderr)
+        f.write("\n".join(logs))
+    if failed:
+        raise RuntimeError(f"nvcc failed for {failed} (see {log_path}):\n" + "\n".join(logs)[-4000:])
+    link = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
+            "-o", out + ".tmp"] + [obj for _, obj, _ in procs]
+    res = subprocess.run(link, capture_output=True, text=True)
     if res.returncode != 0:
-        raise RuntimeError(f"nvcc failed (see {log_path}):\n{res.stderr[-4000:]}")
+        raise RuntimeError(f"link failed:\n{res.stderr[-4000:]}")
     os.replace(out + ".tmp", out)
     return out
 

@@ -19,7 +19,7 @@
 #include <unordered_set>
 #include <vector>
 
-#include "../../include/flatknn.h"
+#include "fk_host.cuh"
 #include "flatknn_kernels.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
@@ -27,12 +27,13 @@
 #include <cub/device/device_select.cuh>
 
 using namespace fk;
+using fkh::set_err;
+using fkh::SMEM_LIMIT;
 
+namespace fkh {
 namespace {
-
 thread_local std::string g_err;
-
-int set_err(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+}
 int set_err(int code, const char* fmt, ...) {
   char buf[512];
   va_list ap;
@@ -42,22 +43,10 @@ int set_err(int code, const char* fmt, ...) {
   g_err = buf;
   return code;
 }
+const char* last_error() { return g_err.c_str(); }
+}  // namespace fkh
 
-#define CK(expr)                                                                                         \
-  do {                                                                                                   \
-    cudaError_t e_ = (expr);                                                                             \
-    if (e_ != cudaSuccess)                                                                               \
-      return set_err(e_ == cudaErrorMemoryAllocation ? FK_E_NOMEM : FK_E_CUDA, "%s failed: %s (%s:%d)", \
-                     #expr, cudaGetErrorString(e_), __FILE__, __LINE__);                                 \
-  } while (0)
-
-#define CKL()                                                                                       \
-  do {                                                                                              \
-    cudaError_t e_ = cudaGetLastError();                                                            \
-    if (e_ != cudaSuccess)                                                                          \
-      return set_err(FK_E_CUDA, "kernel launch failed: %s (%s:%d)", cudaGetErrorString(e_), __FILE__, \
-                     __LINE__);                                                                     \
-  } while (0)
+namespace {
 
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                       const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
@@ -100,7 +89,6 @@ constexpr int64_t FP32_1X_MIN_ROWS = 262144;
 constexpr size_t L2_CHUNK_BYTES = 48ull << 20;  // streamed base per N-chunk (2 chunks in flight << 126 MB L2)
 constexpr size_t PARTIAL_BYTES = 4ull << 30;    // split-N partial top-k lists
 constexpr int MERGE_SMC = 16384;    // large-k merge: survivors gathered in smem (128 KB) + 2048 winners
-constexpr int SMEM_LIMIT = 232448 - 1024;  // sm_100 227 KB per block, minus the static barrier block
 constexpr int SMEM_RESERVE = 1024 /*align*/ + 512 /*barriers + tmem slot*/;
 
 int elem_bytes_of(int storage) { return storage == FK_F32 ? 4 : 2; }
@@ -247,88 +235,18 @@ int launch_prep(int kmode, const void* x, int dtype, int64_t n, int d, int dp, v
 
 size_t dtype_bytes(int dtype) { return dtype == FK_F32 ? 4 : 2; }
 
-template <int MODE, int KQ, bool IP, int EPI, int TBN>
-int launch_fused_tb(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0, const CUtensorMap& b1,
-                    const SearchParams& sp, int grid, int smem, cudaStream_t st) {
-  auto kern = fused_knn_kernel<MODE, KQ, IP, EPI, TBN>;
-  static bool configured = false;  // per instantiation
-  if (!configured) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
-    configured = true;
-  }
-  if (sp.cluster == 2) {  // CTA pairs sharing base tiles (TMA multicast)
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(128 + 32 * EPI);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&cfg, kern, a0, a1, b0, b1, sp));
-  } else {
-    kern<<<grid, 128 + 32 * EPI, smem, st>>>(a0, a1, b0, b1, sp);
-  }
-  CKL();
-  return FK_OK;
-}
-
-// 64-column tiles are instantiated only for each storage's default epilogue
-// width (fp32: 4 warps, 16-bit: 8)
-template <int MODE, int KQ, bool IP, int EPI>
-int launch_fused_t(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0, const CUtensorMap& b1,
-                   const SearchParams& sp, int grid, int smem, cudaStream_t st) {
-  if (sp.bn == 64) {
-    if constexpr ((MODE == 0 || MODE == 4) == (EPI == 4))
-      return launch_fused_tb<MODE, KQ, IP, EPI, 64>(a0, a1, b0, b1, sp, grid, smem, st);
-    return set_err(FK_E_UNSUPPORTED, "64-column tiles need the default epilogue width");
-  }
-  return launch_fused_tb<MODE, KQ, IP, EPI, 128>(a0, a1, b0, b1, sp, grid, smem, st);
-}
-
-template <int MODE, bool IP, int EPI>
-int launch_fused_k(int kq, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
-                   const CUtensorMap& b1, const SearchParams& sp, int grid, int smem, cudaStream_t st) {
-  switch (kq) {
-    case 8: return launch_fused_t<MODE, 8, IP, EPI>(a0, a1, b0, b1, sp, grid, smem, st);
-    case 16: return launch_fused_t<MODE, 16, IP, EPI>(a0, a1, b0, b1, sp, grid, smem, st);
-    case 32: return launch_fused_t<MODE, 32, IP, EPI>(a0, a1, b0, b1, sp, grid, smem, st);
-    case 0: return launch_fused_t<MODE, 0, IP, EPI>(a0, a1, b0, b1, sp, grid, smem, st);
-    case -1:  // range search: default epilogue width only
-      if constexpr ((MODE == 0 || MODE == 4) == (EPI == 4))
-        return launch_fused_t<MODE, -1, IP, EPI>(a0, a1, b0, b1, sp, grid, smem, st);
-      return set_err(FK_E_UNSUPPORTED, "range search runs with the default epilogue width");
-  }
-  return set_err(FK_E_UNSUPPORTED, "queue bucket %d", kq);
-}
-
-template <int EPI>
-int launch_fused_e(int kmode, bool fold, bool ip, int kq, const CUtensorMap& a0, const CUtensorMap& a1,
-                   const CUtensorMap& b0, const CUtensorMap& b1, const SearchParams& sp, int grid, int smem,
-                   cudaStream_t st) {
-  if (kmode == 0)
-    return ip ? launch_fused_k<0, true, EPI>(kq, a0, a1, b0, b1, sp, grid, smem, st)
-              : launch_fused_k<0, false, EPI>(kq, a0, a1, b0, b1, sp, grid, smem, st);
-  if (kmode == 4)
-    return ip ? launch_fused_k<4, true, EPI>(kq, a0, a1, b0, b1, sp, grid, smem, st)
-              : launch_fused_k<4, false, EPI>(kq, a0, a1, b0, b1, sp, grid, smem, st);
-  if (kmode == 1)
-    return ip ? launch_fused_k<1, true, EPI>(kq, a0, a1, b0, b1, sp, grid, smem, st)
-              : launch_fused_k<1, false, EPI>(kq, a0, a1, b0, b1, sp, grid, smem, st);
-  if (fold && !ip) return launch_fused_k<3, false, EPI>(kq, a0, a1, b0, b1, sp, grid, smem, st);
-  return ip ? launch_fused_k<2, true, EPI>(kq, a0, a1, b0, b1, sp, grid, smem, st)
-            : launch_fused_k<2, false, EPI>(kq, a0, a1, b0, b1, sp, grid, smem, st);
-}
-
 int launch_fused(int epi, int kmode, bool fold, bool ip, int kq, const CUtensorMap& a0, const CUtensorMap& a1,
                  const CUtensorMap& b0, const CUtensorMap& b1, const SearchParams& sp, int grid, int smem,
                  cudaStream_t st) {
-  if (epi == 8) return launch_fused_e<8>(kmode, fold, ip, kq, a0, a1, b0, b1, sp, grid, smem, st);
-  return launch_fused_e<4>(kmode, fold, ip, kq, a0, a1, b0, b1, sp, grid, smem, st);
+  using fkh::launch_fused_mode;
+  switch (kmode) {
+    case 0: return launch_fused_mode<0>(epi, ip, kq, a0, a1, b0, b1, sp, grid, smem, st);
+    case 4: return launch_fused_mode<4>(epi, ip, kq, a0, a1, b0, b1, sp, grid, smem, st);
+    case 1: return launch_fused_mode<1>(epi, ip, kq, a0, a1, b0, b1, sp, grid, smem, st);
+    default:
+      if (fold && !ip) return launch_fused_mode<3>(epi, ip, kq, a0, a1, b0, b1, sp, grid, smem, st);
+      return launch_fused_mode<2>(epi, ip, kq, a0, a1, b0, b1, sp, grid, smem, st);
+  }
 }
 
 // Split-N plan: choose the number of N-chunks S so that num_m*S work units
@@ -367,7 +285,7 @@ void plan_split(int num_m, int n_tiles, int num_sms, int min_S, int max_S, int* 
 // =====================================================================  C ABI
 extern "C" {
 
-const char* fk_last_error(void) { return g_err.c_str(); }
+const char* fk_last_error(void) { return fkh::last_error(); }
 
 int fk_create(int device, int d, int metric, int storage, fk_index** out) {
   if (!out) return set_err(FK_E_INVALID, "out is NULL");
@@ -712,14 +630,15 @@ int launch_merge(fk_index* h, const Plan& P, int64_t nq, int k, bool ip, float* 
     int p2 = 1;
     while (p2 < k) p2 <<= 1;
     const size_t msmem = (size_t)(smc + p2) * 8;
-    static bool merge_cfg = false;
-    if (!merge_cfg) {
+    static std::atomic<uint64_t> merge_cfg{0};
+    int rc = fkh::once_per_device(merge_cfg, []() -> int {
       CK(cudaFuncSetAttribute(merge_large_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (MERGE_SMC + FK_MAX_K) * 8));
       CK(cudaFuncSetAttribute(merge_large_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (MERGE_SMC + FK_MAX_K) * 8));
-      merge_cfg = true;
-    }
+      return FK_OK;
+    });
+    if (rc) return rc;
     const int* pc = P.kq == 0 ? static_cast<const int*>(h->pcnt.p) : nullptr;  // queue lists: k entries each
     const uint32_t* thr = static_cast<const uint32_t*>(h->thr.p);
     if (ip)
@@ -799,14 +718,15 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
   const int smc = std::min(MERGE_SMC, std::max(1024, 8 * kp));
   int p2 = 1;
   while (p2 < k) p2 <<= 1;
-  static bool cfg = false;
-  if (!cfg) {
-    CK(cudaFuncSetAttribute(merge_rescore_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (MERGE_SMC + FK_MAX_K) * 8));
-    CK(cudaFuncSetAttribute(merge_rescore_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (MERGE_SMC + FK_MAX_K) * 8));
-    cfg = true;
-  }
+  static std::atomic<uint64_t> cfg{0};
+  if ((rc = fkh::once_per_device(cfg, []() -> int {
+         CK(cudaFuncSetAttribute(merge_rescore_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (MERGE_SMC + FK_MAX_K) * 8));
+         CK(cudaFuncSetAttribute(merge_rescore_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (MERGE_SMC + FK_MAX_K) * 8));
+         return FK_OK;
+       })))
+    return rc;
   const size_t msmem = (size_t)(smc + p2) * 8;
   const auto pk = static_cast<const uint32_t*>(h->pkey.p);
   const auto pp = static_cast<const uint32_t*>(h->ppos.p);
@@ -843,12 +763,13 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
   // scratch of one exact composite per row per slot: <= 8 slots, <= 512 MB
   const int nslots = (int)std::max<int64_t>(1, std::min<int64_t>({nq, 8, (512ll << 20) / (h->ntotal * 8)}));
   if ((rc = h->rcomp.ensure((size_t)nslots * h->ntotal * 8))) return rc;
-  static bool fcfg = false;
-  if (!fcfg) {
-    CK(cudaFuncSetAttribute(fallback_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, FK_MAX_K * 8));
-    CK(cudaFuncSetAttribute(fallback_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, FK_MAX_K * 8));
-    fcfg = true;
-  }
+  static std::atomic<uint64_t> fcfg{0};
+  if ((rc = fkh::once_per_device(fcfg, []() -> int {
+         CK(cudaFuncSetAttribute(fallback_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, FK_MAX_K * 8));
+         CK(cudaFuncSetAttribute(fallback_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, FK_MAX_K * 8));
+         return FK_OK;
+       })))
+    return rc;
   auto comp = static_cast<uint64_t*>(h->rcomp.p);
   const size_t ssm = (size_t)p2 * 8;
   if (ip)
@@ -1274,7 +1195,19 @@ int fk_remove_ids(fk_index* h, const int64_t* ids, int64_t n, int on_device, int
 
 int fk_set_profiling(fk_index* h, int on) {
   if (!h) return set_err(FK_E_INVALID, "NULL index");
-  h->profiling = on;
+  std::lock_guard<std::mutex> g(h->mu);
+  if (on > 0) {
+    // create the event pool up front (on = searches to reserve): event
+    // creation inside a timed loop costs driver calls that can stall it
+    CK(cudaSetDevice(h->device));
+    const size_t want = h->ev_used + (size_t)std::max(on, 64);
+    while (h->ev_pool.size() < want) {
+      std::array<cudaEvent_t, 4> q{};
+      for (auto& e : q) CK(cudaEventCreate(&e));
+      h->ev_pool.push_back(q);
+    }
+  }
+  h->profiling = on > 0;
   return FK_OK;
 }
 

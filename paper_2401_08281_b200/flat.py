@@ -217,8 +217,10 @@ class FlatIndex(Index):
         return self._search(as_vectors(q, self.d), int(k), with_positions=True)
 
     # ------------------------------------------------------------------ instrumentation
-    def set_profiling(self, on: bool) -> None:
-        N.check(N.lib().fk_set_profiling(self._h, int(on)))
+    def set_profiling(self, on: bool, reserve: int = 64) -> None:
+        """Record CUDA events around the kernels of each search; the events of
+        ``reserve`` searches are created now (none inside a timed loop)."""
+        N.check(N.lib().fk_set_profiling(self._h, max(1, int(reserve)) if on else 0))
 
     def kernel_times(self):
         """(prep_ms, fused_ms, merge_ms), launches of the last search."""
