@@ -46,7 +46,8 @@ typedef struct fk_index fk_index;
 #define FK_METRIC_L2 1
 
 /* storage / input dtypes */
-#define FK_F32 0  /* storage: fp32, searched with a 3xTF32 split (fp32-faithful) */
+#define FK_F32 0  /* storage: fp32 (hi/lo tf32 split kept; k <= 16 over >= 256k rows: one tf32
+                     pass + certified exact fp32 rescoring, else 3xTF32; fp32-faithful) */
 #define FK_F16 1  /* storage: fp16 (RNE from f32), tensor-core kind::f16      */
 #define FK_BF16 2 /* storage: bf16 (RNE from f32), tensor-core kind::f16      */
 
@@ -68,7 +69,9 @@ int fk_create(int device, int d, int metric, int storage, fk_index** out);
 int fk_add(fk_index* h, const void* x, int64_t n, int dtype, const int64_t* ids, int on_device,
            void* stream);
 
-/* Exact top-k for nq queries (row-major nq x d of `dtype`).
+/* Exact top-k for nq queries (row-major nq x d of `dtype`); FlatIndex._search
+ * dispatch: nq >= FK_OPT_BLAS_THRESHOLD -> the fused GEMM + top-k path
+ * (flat_search_blas semantics), else the direct per-pair path (flat_search).
  * D: nq x k float32 distances (L2: squared, clamped at 0; IP: inner product).
  * I: nq x k int64 ids (-1 for padding).
  * P: optional (may be NULL) nq x k int64 storage positions (-1 for padding),
@@ -119,11 +122,29 @@ int fk_kernel_times(fk_index* h, float* ms3, int* nlaunch);
  * every stored vector with direct distance <= radius (L2) or inner product
  * >= radius (IP), per query sorted best first with ties by smaller id
  * (flat.py:137).  Writes lims [nq + 1] (CSR offsets, host or device) and the
- * entry count to *total; the entries stay in the handle until
- * fk_range_fetch copies ids [total] (int64) and distances [total] (f32). */
+ * entry count to *total, and returns the entries in a per-call result object
+ * *out (caller-owned: fk_range_fetch copies them, fk_range_free releases it),
+ * so concurrent range searches on one index never mix their results. */
+typedef struct fk_range_result fk_range_result;
 int fk_range_search(fk_index* h, const void* q, int64_t nq, int dtype, float radius, int64_t* lims, int64_t* total,
-                    int on_device, void* stream);
-int fk_range_fetch(fk_index* h, int64_t* ids, float* dist, int on_device, void* stream);
+                    fk_range_result** out, int on_device, void* stream);
+/* Copy ids [total] (int64) and distances [total] (f32); capacity = entries
+ * the output arrays hold (FK_E_INVALID when smaller than total). */
+int fk_range_fetch(fk_range_result* r, int64_t* ids, float* dist, int64_t capacity, int on_device, void* stream);
+int64_t fk_range_total(const fk_range_result* r);
+void fk_range_free(fk_range_result* r);
+
+/* Per-index options.
+ * FK_OPT_PLAN_ROWS: database rows the fp32 algorithm choice is made for
+ * (0 = the index's own ntotal).  A shard of a row-sharded index passes the
+ * global row count so every shard runs the algorithm the unsharded search
+ * would (ShardedFlatIndex does). */
+#define FK_OPT_PLAN_ROWS 1
+/* FK_OPT_BLAS_THRESHOLD: batches of fewer queries take the direct path
+ * (exact per-pair distances, flat.py:58-62 -> flat_search flat.py:76-91);
+ * default 20 = annkit config.blas_threshold (config.py:9); 0 disables it. */
+#define FK_OPT_BLAS_THRESHOLD 2
+int fk_set_option(fk_index* h, int option, int64_t value);
 
 /* k-means assignment in fp64 (replaces annkit quantize.py:38-62 `_assign`,
  * the Lloyd-iteration / IVF-training consumer of the flat path).

@@ -17,6 +17,18 @@ It restates, in plain numpy, the reference annkit BLAS search path
 * ``knn_recall``        <- ``pkg/src/annkit/core.py:314-327``
 * ``flat_range_search`` <- ``pkg/src/annkit/flat.py:121-144`` (direct pairwise
                            distances, <= radius / >= for IP, (value, id) order)
+* ``flat_search_direct``<- ``pkg/src/annkit/flat.py:76-91`` (flat_search: the
+                           direct path FlatIndex._search takes for batches below
+                           config.blas_threshold, flat.py:58-62) with pairwise
+                           -> dist_one (``_ckernels.pyx:49-57``): L2 sum (q-x)^2,
+                           IP sum q x, here accumulated in fp64 and rounded once
+* ``merge_topk``        <- the total order of ``core.py:205-236`` (64-bit key
+                           ``monotone(value) << 32 | column``) applied to the
+                           union of per-shard top-k lists carrying GLOBAL
+                           columns: equals ``topk_rows`` over the concatenated
+                           rows (each shard's top-k holds every global top-k
+                           member of that shard).  Used to evaluate the oracle
+                           over a large database shard by shard.
 
 Parity pinning: ``tests/test_oracle.py`` checks this restatement against the
 golden vectors in ``tests/golden/`` that ``tests/golden/make_golden.py``
@@ -73,6 +85,28 @@ def topk_rows(distances: np.ndarray, k: int, descending: bool = False):
     return top_ids, top_vals
 
 
+def merge_topk(parts, k: int, descending: bool = False):
+    """Merge per-shard (global positions (nq, k_s) int64, values (nq, k_s) f32)
+    lists into the top-k under the reference's (value, column) order
+    (core.py:205-236); -1 / worst padding as topk_rows."""
+    pos = np.concatenate([p for p, _ in parts], axis=1)
+    vals = np.concatenate([v for _, v in parts], axis=1).astype(np.float32)
+    nq = pos.shape[0]
+    key_vals = -vals if descending else vals
+    keys = (monotone_key(key_vals).astype(np.uint64) << np.uint64(32)) | pos.astype(np.uint64)
+    keys = np.where(pos >= 0, keys, np.uint64(0xFFFFFFFFFFFFFFFF))
+    order = np.argsort(keys, axis=1, kind="stable")[:, :k]
+    out_pos = np.take_along_axis(pos, order, axis=1)
+    out_val = np.take_along_axis(vals, order, axis=1)
+    if out_pos.shape[1] < k:
+        pad = k - out_pos.shape[1]
+        out_pos = np.hstack([out_pos, np.full((nq, pad), -1, np.int64)])
+        out_val = np.hstack([out_val, np.full((nq, pad), np.nan, np.float32)])
+    worst = np.float32(-np.inf) if descending else np.float32(np.inf)
+    out_val = np.where(out_pos >= 0, out_val, worst).astype(np.float32)
+    return out_pos.astype(np.int64), out_val
+
+
 def add_norms(xb: np.ndarray) -> np.ndarray:
     """Squared norms of stored vectors, f32 einsum (flat.py:31)."""
     xb = np.ascontiguousarray(xb, dtype=np.float32)
@@ -122,6 +156,29 @@ def flat_search_blas(xb: np.ndarray, q: np.ndarray, k: int, metric: str = METRIC
         all_ids[lo:hi] = pos
         all_dist[lo:hi] = vals
     return finish(ids, all_ids, nb), all_dist
+
+
+def flat_search_direct(xb: np.ndarray, q: np.ndarray, k: int, metric: str = METRIC_L2,
+                       ids: np.ndarray | None = None, rows: int = 4096):
+    """Direct-path top-k (flat.py:76-91): per-pair direct distances in fp64
+    (difference form for L2), rounded to fp32, ranked by ``topk_rows``."""
+    xb = np.ascontiguousarray(xb, dtype=np.float32)
+    q = np.atleast_2d(np.ascontiguousarray(q, dtype=np.float32))
+    nq, nb = q.shape[0], xb.shape[0]
+    q64 = q.astype(np.float64)
+    dmat = np.empty((nq, nb), dtype=np.float32)
+    with np.errstate(invalid="ignore", over="ignore"):
+        for lo in range(0, nb, rows):
+            x64 = xb[lo:lo + rows].astype(np.float64)
+            if metric == METRIC_L2:
+                d = ((q64[:, None, :] - x64[None, :, :]) ** 2).sum(-1)
+            else:
+                d = q64 @ x64.T
+            dmat[:, lo:lo + rows] = d.astype(np.float32)
+    if ids is None:
+        ids = np.arange(nb, dtype=np.int64)
+    pos, vals = topk_rows(dmat, k, metric == METRIC_IP)
+    return finish(ids, pos, nb), vals
 
 
 def flat_search_exact(xb: np.ndarray, q: np.ndarray, k: int, metric: str = METRIC_L2):

@@ -7,6 +7,7 @@ The compute runs in hand-written sm_100a kernels (tcgen05 GEMM + fused
 top-k) behind the C ABI declared in ``include/flatknn.h``.
 """
 
+from . import config
 from .core import (METRIC_IP, METRIC_L2, Index, Metric, MetricKind, RangeResult, SearchResult, as_vectors,
                    knn_recall)
 from .flat import FlatIndex, IndexFlatIP, IndexFlatL2
@@ -28,6 +29,7 @@ __all__ = [
     "SearchResult",
     "ShardedFlatIndex",
     "as_vectors",
+    "config",
     "assign_vectors",
     "coarse_quantizer",
     "kmeans_assign",

@@ -28,8 +28,11 @@ EXPORTED = (
     "fk_create", "fk_add", "fk_search", "fk_merge_shards", "fk_reconstruct", "fk_remove_ids",
     "fk_reset", "fk_ntotal", "fk_dim", "fk_get_ids", "fk_destroy", "fk_last_error",
     "fk_set_profiling", "fk_kernel_times", "fk_last_plan", "fk_kmeans_rescore",
-    "fk_range_search", "fk_range_fetch",
+    "fk_range_search", "fk_range_fetch", "fk_range_total", "fk_range_free", "fk_set_option",
 )
+
+FK_OPT_PLAN_ROWS = 1
+FK_OPT_BLAS_THRESHOLD = 2
 
 _lib = None
 
@@ -53,8 +56,12 @@ _SIGS = {
     "fk_set_profiling": (_INT, [_P, _INT]),
     "fk_kernel_times": (_INT, [_P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(_INT)]),
     "fk_last_plan": (_INT, [_P, ctypes.POINTER(_INT)]),
-    "fk_range_search": (_INT, [_P, _P, _I64, _INT, ctypes.c_float, _P, ctypes.POINTER(_I64), _INT, _P]),
-    "fk_range_fetch": (_INT, [_P, _P, _P, _INT, _P]),
+    "fk_range_search": (_INT, [_P, _P, _I64, _INT, ctypes.c_float, _P, ctypes.POINTER(_I64), ctypes.POINTER(_P),
+                               _INT, _P]),
+    "fk_range_fetch": (_INT, [_P, _P, _P, _I64, _INT, _P]),
+    "fk_range_total": (_I64, [_P]),
+    "fk_range_free": (None, [_P]),
+    "fk_set_option": (_INT, [_P, _INT, _I64]),
     "fk_kmeans_rescore": (_INT, [_P, _I64, _INT, _P, _P, _I64, _P, _INT, _INT, _P, ctypes.c_double,
                                  ctypes.c_double, _P, _P, _P, _P]),
     "fk_debug_set_ip_dump": (_INT, [_P, _P]),

@@ -105,6 +105,8 @@ struct DevBuf {
   }
   int ensure(size_t want) {
     if (want <= bytes) return FK_OK;
+    // growth is rare: wait for every stream that may still read the old buffer
+    if (p) cudaDeviceSynchronize();
     release();
     size_t b = std::max<size_t>(want, 256);
     cudaError_t e = cudaMalloc(&p, b);
@@ -133,12 +135,17 @@ struct fk_index {
   // range search: candidates, exact pass, sort scratch and the CSR result
   DevBuf rfail, rcomp, rflag, glock, gkeys;
   unsigned int* inexact = nullptr;  // device {base, queries}: a value with a nonzero lo part was stored/staged  // fp32 MODE 4: per-query certification flags, exact-fallback composites
-  DevBuf rcand, rcount, rdist, rkid, rkrd, rkeep, rrowc, rsel, rnsel, rtmp, rkid2, rkrd2, rv1, rv2, rlims, rids,
-      rdist_out;
+  DevBuf rcand, rcount, rdist, rkid, rkrd, rkeep, rrowc, rsel, rnsel, rtmp, rkid2, rkrd2, rv1, rv2, rlims;
+  // every call that touches the handle's scratch or storage waits for the
+  // previous such call's stream work (stream-ordered reuse: concurrent
+  // searches on different streams stay correct) and records this event
+  cudaEvent_t scratch_ev = nullptr;
+  bool scratch_used = false;
+  int64_t plan_rows = 0;  // FK_OPT_PLAN_ROWS (0: ntotal)
+  int64_t blas_threshold = 20;  // FK_OPT_BLAS_THRESHOLD (reference config.py:9)
   float r_radius = 0.f;
   int r_kfinal = 0;  // MODE 4 search: the caller's k (lists keep k' >= k)
   bool r_union = false;  // MODE 4 search: maintain the per-query running union bound
-  int64_t r_total = 0, r_nq = 0;
   unsigned long long r_cap = 0;
   long long est_fallbacks = 0;  // large-k searches whose estimated bound failed certification
   std::mutex mu;
@@ -155,6 +162,13 @@ struct fk_index {
   unsigned long long* trace = nullptr;  // debug timeline hook
 };
 
+// Entries of one range search (owned by the caller until fk_range_free).
+struct fk_range_result {
+  int device = 0;
+  int64_t total = 0;
+  DevBuf ids, dist;
+};
+
 namespace {
 
 cudaEvent_t* next_events(fk_index* h) {
@@ -168,6 +182,17 @@ cudaEvent_t* next_events(fk_index* h) {
 }
 
 size_t row_bytes(const fk_index* h) { return (size_t)h->dp * elem_bytes_of(h->storage); }
+
+// Stream ordering of the handle's scratch (see fk_index::scratch_ev).
+int scratch_begin(fk_index* h, cudaStream_t st) {
+  if (h->scratch_used) CK(cudaStreamWaitEvent(st, h->scratch_ev, 0));
+  return FK_OK;
+}
+int scratch_end(fk_index* h, cudaStream_t st) {
+  CK(cudaEventRecord(h->scratch_ev, st));
+  h->scratch_used = true;
+  return FK_OK;
+}
 
 int grow(fk_index* h, int64_t need, cudaStream_t st) {
   if (need <= h->cap) return FK_OK;
@@ -196,7 +221,7 @@ int grow(fk_index* h, int64_t need, cudaStream_t st) {
     CK(cudaMemcpyAsync(nn, h->norms, h->ntotal * sizeof(float), cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpyAsync(ni, h->ids, h->ntotal * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
   }
-  CK(cudaStreamSynchronize(st));
+  CK(cudaDeviceSynchronize());  // in-flight searches on any stream may read the old storage
   cudaFree(h->s0);
   cudaFree(h->s1);
   cudaFree(h->norms);
@@ -325,7 +350,10 @@ int fk_create(int device, int d, int metric, int storage, fk_index** out) {
   h->num_sms = prop.multiProcessorCount;
   if (cudaMalloc((void**)&h->inexact, 2 * sizeof(unsigned int)) != cudaSuccess ||
       cudaMemset(h->inexact, 0, 2 * sizeof(unsigned int)) != cudaSuccess ||
-      cudaMalloc((void**)&h->xn_max, sizeof(float)) != cudaSuccess || cudaMemset(h->xn_max, 0, sizeof(float)) != cudaSuccess) {
+      cudaMalloc((void**)&h->xn_max, sizeof(float)) != cudaSuccess || cudaMemset(h->xn_max, 0, sizeof(float)) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->scratch_ev, cudaEventDisableTiming) != cudaSuccess) {
+    cudaFree(h->inexact);
+    cudaFree(h->xn_max);
     delete h;
     return set_err(FK_E_NOMEM, "cudaMalloc failed");
   }
@@ -342,9 +370,12 @@ void fk_destroy(fk_index* h) {
   cudaFree(h->s1);
   cudaFree(h->norms);
   cudaFree(h->ids);
-  for (DevBuf* b : {&h->q_in, &h->q0, &h->q1, &h->qn, &h->pkey, &h->ppos, &h->thr, &h->pcnt, &h->cbuf, &h->fail, &h->outD, &h->outI, &h->outP,
-                    &h->stage_in, &h->stage_ids})
+  for (DevBuf* b : {&h->q_in, &h->q0, &h->q1, &h->qn, &h->pkey, &h->ppos, &h->thr, &h->pcnt, &h->cbuf, &h->fail,
+                    &h->outD, &h->outI, &h->outP, &h->stage_in, &h->stage_ids, &h->rfail, &h->rcomp, &h->rflag,
+                    &h->glock, &h->gkeys, &h->rcand, &h->rcount, &h->rdist, &h->rkid, &h->rkrd, &h->rkeep,
+                    &h->rrowc, &h->rsel, &h->rnsel, &h->rtmp, &h->rkid2, &h->rkrd2, &h->rv1, &h->rv2, &h->rlims})
     b->release();
+  if (h->scratch_ev) cudaEventDestroy(h->scratch_ev);
   cudaFree(h->xn_max);
   cudaFree(h->inexact);
   for (auto& q : h->ev_pool)
@@ -376,8 +407,9 @@ int fk_add(fk_index* h, const void* x, int64_t n, int dtype, const int64_t* ids,
   std::lock_guard<std::mutex> g(h->mu);
   CK(cudaSetDevice(h->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  int rc = grow(h, h->ntotal + n, st);
+  int rc = scratch_begin(h, st);
   if (rc) return rc;
+  if ((rc = grow(h, h->ntotal + n, st))) return rc;
   const size_t eb = dtype_bytes(dtype);
   const size_t in_row = (size_t)h->d * eb;
   // stage host input in <= 256 MB slices
@@ -405,6 +437,7 @@ int fk_add(fk_index* h, const void* x, int64_t n, int dtype, const int64_t* ids,
   norm_max_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, st>>>(
       h->norms + h->ntotal, n, reinterpret_cast<unsigned int*>(h->xn_max));
   CKL();
+  if ((rc = scratch_end(h, st))) return rc;
   if (!on_device) CK(cudaStreamSynchronize(st));
   h->ntotal += n;
   return FK_OK;
@@ -759,9 +792,11 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
     CK(cudaStreamSynchronize(st));
     fprintf(stderr, "[fk] mode4 k=%d k'=%d nq=%lld uncertified=%d\n", k, kp, (long long)nq, nf);
   }
-  // uncertified queries: exact fallback on the device (no host sync)
-  // scratch of one exact composite per row per slot: <= 8 slots, <= 512 MB
-  const int nslots = (int)std::max<int64_t>(1, std::min<int64_t>({nq, 8, (512ll << 20) / (h->ntotal * 8)}));
+  // uncertified queries: exact fallback on the device (no host sync); up to
+  // one wave of CTAs, each scanning the base for its failed queries, with a
+  // scratch slot of one exact composite per row (<= 2 GB of slots)
+  const int nslots = (int)std::max<int64_t>(
+      1, std::min<int64_t>({nq, (int64_t)h->num_sms, (2048ll << 20) / (h->ntotal * 8)}));
   if ((rc = h->rcomp.ensure((size_t)nslots * h->ntotal * 8))) return rc;
   static std::atomic<uint64_t> fcfg{0};
   if ((rc = fkh::once_per_device(fcfg, []() -> int {
@@ -780,6 +815,47 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
                                                      h->ids, dD, dI, dP, comp);
   CKL();
   h->nlaunch++;
+  return FK_OK;
+}
+
+// Direct path (flat.py:58-62 -> flat_search flat.py:76-91) for batches
+// below the BLAS threshold: exact direct distances of every (query, row),
+// then a per-query top-k selection.  Queries are staged already.
+int search_direct(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI, int64_t* dP, cudaEvent_t* ev,
+                  cudaStream_t st) {
+  int rc;
+  const int64_t n = h->ntotal;
+  if (n > (int64_t)INT32_MAX) return set_err(FK_E_UNSUPPORTED, "direct path over more than 2^31 rows");
+  const int64_t group = std::max<int64_t>(1, std::min<int64_t>(nq, (2048ll << 20) / (n * 8)));
+  if ((rc = h->rcomp.ensure((size_t)group * n * 8))) return rc;
+  auto comp = static_cast<uint64_t*>(h->rcomp.p);
+  int p2 = 1;
+  while (p2 < k) p2 <<= 1;
+  const size_t qrow = row_bytes(h);
+  const int mode = h->storage == FK_F32 ? (h->split == 2 ? 0 : 4) : (h->storage == FK_F16 ? 1 : 2);
+  if (ev) CK(cudaEventRecord(ev[1], st));
+  for (int64_t g0 = 0; g0 < nq; g0 += group) {
+    const int gq = (int)std::min(group, nq - g0);
+    const void* qa = static_cast<const uint8_t*>(h->q0.p) + (size_t)g0 * qrow;
+    const void* qb = h->split == 2 ? static_cast<const uint8_t*>(h->q1.p) + (size_t)g0 * qrow : nullptr;
+    const unsigned grid = (unsigned)((n + 7) / 8);
+    if (mode == 0)
+      direct_dist_kernel<0><<<grid, 256, 0, st>>>(qa, qb, gq, h->s0, h->s1, n, h->d, h->dp, ip, 0, comp);
+    else if (mode == 4)
+      direct_dist_kernel<4><<<grid, 256, 0, st>>>(qa, nullptr, gq, h->s0, nullptr, n, h->d, h->dp, ip, 0, comp);
+    else if (mode == 1)
+      direct_dist_kernel<1><<<grid, 256, 0, st>>>(qa, nullptr, gq, h->s0, nullptr, n, h->d, h->dp, ip, 0, comp);
+    else
+      direct_dist_kernel<2><<<grid, 256, 0, st>>>(qa, nullptr, gq, h->s0, nullptr, n, h->d, h->dp, ip, h->fold, comp);
+    CKL();
+    if (ev && g0 == 0) CK(cudaEventRecord(ev[2], st));
+    if (ip)
+      direct_select_kernel<true><<<gq, 256, (size_t)p2 * 8, st>>>(comp, n, (int)g0, k, h->ids, dD, dI, dP);
+    else
+      direct_select_kernel<false><<<gq, 256, (size_t)p2 * 8, st>>>(comp, n, (int)g0, k, h->ids, dD, dI, dP);
+    CKL();
+    h->nlaunch += 2;
+  }
   return FK_OK;
 }
 
@@ -812,11 +888,12 @@ __global__ void counts_to_i64_kernel(const unsigned int* __restrict__ c, int64_t
 extern "C" {
 
 int fk_range_search(fk_index* h, const void* q, int64_t nq, int dtype, float radius, int64_t* lims, int64_t* total,
-                    int on_device, void* stream) {
+                    fk_range_result** out, int on_device, void* stream) {
   if (!h) return set_err(FK_E_INVALID, "NULL index");
   if (nq < 0) return set_err(FK_E_INVALID, "nq must be >= 0");
   if (dtype != FK_F32 && dtype != FK_F16 && dtype != FK_BF16) return set_err(FK_E_INVALID, "bad dtype %d", dtype);
-  if (!lims || !total) return set_err(FK_E_INVALID, "NULL output pointer");
+  if (!lims || !total || !out) return set_err(FK_E_INVALID, "NULL output pointer");
+  *out = nullptr;
   if (nq > (int64_t)INT32_MAX / 2) return set_err(FK_E_UNSUPPORTED, "nq too large for one call");
   if (nq > 0 && !q) return set_err(FK_E_INVALID, "NULL query pointer");
   std::lock_guard<std::mutex> g(h->mu);
@@ -824,8 +901,15 @@ int fk_range_search(fk_index* h, const void* q, int64_t nq, int dtype, float rad
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool ip = h->metric == FK_METRIC_IP;
   int rc;
-  h->r_total = 0;
-  h->r_nq = nq;
+  if ((rc = scratch_begin(h, st))) return rc;
+  // the entries go to a per-call result object (no state left in the handle
+  // between the two calls: concurrent range searches cannot mix results)
+  fk_range_result* res = new fk_range_result();
+  res->device = h->device;
+  struct Guard {
+    fk_range_result*& r;
+    ~Guard() { fk_range_free(r); }
+  } guard{res};
   if ((rc = h->rlims.ensure((size_t)(nq + 1) * sizeof(int64_t)))) return rc;
   int64_t* dlims = static_cast<int64_t*>(h->rlims.p);
   if (nq == 0 || h->ntotal == 0) {  // flat.py:124-125: empty lists
@@ -912,12 +996,12 @@ int fk_range_search(fk_index* h, const void* q, int64_t nq, int dtype, float rad
       gather_u64_kernel<<<g, 256, 0, st>>>(v1, krd, nsel, kid2);
       CKL();
       CK(cub::DeviceRadixSort::SortPairs(h->rtmp.p, tb2, kid2, krd2, v1, v2, nsel, 0, 32 + row_bits, st));
-      if ((rc = h->rids.ensure(nsel * 8)) || (rc = h->rdist_out.ensure(nsel * 4))) return rc;
-      gather_range_kernel<<<g, 256, 0, st>>>(v2, kid, rd, nsel, static_cast<int64_t*>(h->rids.p),
-                                             static_cast<float*>(h->rdist_out.p));
+      if ((rc = res->ids.ensure(nsel * 8)) || (rc = res->dist.ensure(nsel * 4))) return rc;
+      gather_range_kernel<<<g, 256, 0, st>>>(v2, kid, rd, nsel, static_cast<int64_t*>(res->ids.p),
+                                             static_cast<float*>(res->dist.p));
       CKL();
     }
-    h->r_total = nsel;
+    res->total = nsel;
     // lims = exclusive scan of the per-row survivor counts (nq + 1 entries)
     if ((rc = h->rv1.ensure((size_t)(nq + 1) * 8))) return rc;
     auto cnt64 = static_cast<int64_t*>(h->rv1.p);
@@ -930,23 +1014,54 @@ int fk_range_search(fk_index* h, const void* q, int64_t nq, int dtype, float rad
   }
   CK(cudaMemcpyAsync(lims, dlims, (size_t)(nq + 1) * sizeof(int64_t),
                      on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+  if ((rc = scratch_end(h, st))) return rc;
   CK(cudaStreamSynchronize(st));
-  *total = h->r_total;
+  *total = res->total;
+  *out = res;
+  res = nullptr;  // ownership passes to the caller
   return FK_OK;
 }
 
-int fk_range_fetch(fk_index* h, int64_t* ids, float* dist, int on_device, void* stream) {
-  if (!h) return set_err(FK_E_INVALID, "NULL index");
-  std::lock_guard<std::mutex> g(h->mu);
-  if (h->r_total == 0) return FK_OK;
+int fk_range_fetch(fk_range_result* r, int64_t* ids, float* dist, int64_t capacity, int on_device, void* stream) {
+  if (!r) return set_err(FK_E_INVALID, "NULL range result");
+  if (r->total == 0) return FK_OK;
   if (!ids || !dist) return set_err(FK_E_INVALID, "NULL output pointer");
-  CK(cudaSetDevice(h->device));
+  if (capacity < r->total)
+    return set_err(FK_E_INVALID, "output capacity %lld < %lld range entries", (long long)capacity,
+                   (long long)r->total);
+  CK(cudaSetDevice(r->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-  CK(cudaMemcpyAsync(ids, h->rids.p, (size_t)h->r_total * sizeof(int64_t), kind, st));
-  CK(cudaMemcpyAsync(dist, h->rdist_out.p, (size_t)h->r_total * sizeof(float), kind, st));
+  CK(cudaMemcpyAsync(ids, r->ids.p, (size_t)r->total * sizeof(int64_t), kind, st));
+  CK(cudaMemcpyAsync(dist, r->dist.p, (size_t)r->total * sizeof(float), kind, st));
   CK(cudaStreamSynchronize(st));
   return FK_OK;
+}
+
+int64_t fk_range_total(const fk_range_result* r) { return r ? r->total : -1; }
+
+void fk_range_free(fk_range_result* r) {
+  if (!r) return;
+  cudaSetDevice(r->device);
+  r->ids.release();
+  r->dist.release();
+  delete r;
+}
+
+int fk_set_option(fk_index* h, int option, int64_t value) {
+  if (!h) return set_err(FK_E_INVALID, "NULL index");
+  std::lock_guard<std::mutex> g(h->mu);
+  switch (option) {
+    case FK_OPT_PLAN_ROWS:
+      if (value < 0) return set_err(FK_E_INVALID, "plan rows must be >= 0");
+      h->plan_rows = value;
+      return FK_OK;
+    case FK_OPT_BLAS_THRESHOLD:
+      if (value < 0) return set_err(FK_E_INVALID, "blas threshold must be >= 0");
+      h->blas_threshold = value;
+      return FK_OK;
+  }
+  return set_err(FK_E_INVALID, "unknown option %d", option);
 }
 
 int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D, int64_t* I, int64_t* P,
@@ -965,6 +1080,7 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
   const bool ip = h->metric == FK_METRIC_IP;
   const size_t nout = (size_t)nq * k;
   int rc;
+  if ((rc = scratch_begin(h, st))) return rc;
   h->nlaunch = 0;
   cudaEvent_t* ev = nullptr;
   if (h->profiling && h->ntotal > 0 && !(ev = next_events(h))) return set_err(FK_E_CUDA, "cudaEventCreate failed");
@@ -988,8 +1104,17 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
                                                                          ip ? -INFINITY : INFINITY);
     CKL();
     h->nlaunch = 1;
+  } else if (nq < h->blas_threshold) {  // flat.py:58-62: small batches take the direct path
+    if (ev) CK(cudaEventRecord(ev[0], st));
+    if ((rc = stage_queries(h, q, nq, dtype, on_device, st))) return rc;
+    h->nlaunch++;
+    if ((rc = search_direct(h, nq, k, ip, dD, dI, dP, ev, st))) return rc;
+    if (ev) CK(cudaEventRecord(ev[3], st));
+    std::memset(h->plan, 0, sizeof(h->plan));
+    h->plan[11] = -1;  // direct path
   } else if (h->storage == FK_F32 &&
-             (h->split == 1 || (k <= 16 && h->ntotal >= FP32_1X_MIN_ROWS && !getenv("FK_FP32_3X")))) {
+             (h->split == 1 ||
+              (k <= 16 && (h->plan_rows > 0 ? h->plan_rows : h->ntotal) >= FP32_1X_MIN_ROWS && !getenv("FK_FP32_3X")))) {
     if (ev) CK(cudaEventRecord(ev[0], st));
     if ((rc = stage_queries(h, q, nq, dtype, on_device, st))) return rc;
     h->nlaunch++;
@@ -1081,8 +1206,9 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
     CK(cudaMemcpyAsync(D, dD, nout * sizeof(float), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(I, dI, nout * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     if (P) CK(cudaMemcpyAsync(P, dP, nout * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
   }
+  if ((rc = scratch_end(h, st))) return rc;
+  if (!on_device) CK(cudaStreamSynchronize(st));
   h->nlaunch_acc += h->nlaunch;
   return FK_OK;
 }

@@ -380,9 +380,11 @@ __global__ void __launch_bounds__(256) merge_rescore_kernel(
   // certification on the tf32 values
   const float qn = qnorm[q];
   // band 2e with a 2x safety factor: L2 2 * 2 * 2^-8, IP 2 * 2 * 2^-9 (|q| max|x|)
+  // for tf32 rounding; plus the fp32 accumulation slack (4 dp + 8) 2^-23 (qn + max xn)
+  // (same bound as the fused kernel's band4)
   const bool tf32_exact = inexact != nullptr && (inexact[0] | inexact[1]) == 0u;
   const float e2 = (tf32_exact ? 0.f : (IS_IP ? 0.0078125f : 0.015625f)) * sqrtf(fmaxf(qn, 0.f) * fmaxf(*xn_max, 0.f)) +
-                   (float)dp * 1.1920928955078125e-07f * (fmaxf(qn, 0.f) + fmaxf(*xn_max, 0.f));
+                   (4.f * (float)dp + 8.f) * 1.1920928955078125e-07f * (fmaxf(qn, 0.f) + fmaxf(*xn_max, 0.f));
   bool ok = true;
   uint32_t band_key = 0xFFFFFFFFu;  // only entries with t <= t_k + band can be in the exact top-k
   if (n >= k) {
@@ -487,6 +489,64 @@ __global__ void __launch_bounds__(256) merge_rescore_kernel(
   }
 }
 
+// Exact top-k of one query from its n composites (key << 32 | position):
+// block radix select of the k-th, compaction, bitonic sort of the winners,
+// then (distance, id, position) rows with -1 / worst padding.  All threads of
+// the CTA call it; win holds >= pow2(k) entries.
+template <bool IS_IP>
+__device__ void block_select_write(const uint64_t* comp, int nn, int k, int q, uint64_t* win, int* count,
+                                   uint32_t* hist, uint32_t* sel, const int64_t* __restrict__ ids,
+                                   float* __restrict__ D, int64_t* __restrict__ I, int64_t* __restrict__ P) {
+  const int tid = threadIdx.x;
+  if (tid == 0) *count = 0;
+  __syncthreads();
+  int nw;
+  if (nn <= k) {
+    for (int i = tid; i < nn; i += blockDim.x) win[i] = comp[i];
+    nw = nn;
+  } else {
+    const uint64_t kth = block_kth([&](int e) { return comp[e]; }, nn, (uint32_t)k, hist, sel);
+    for (int i = tid; i < nn; i += blockDim.x)
+      if (comp[i] <= kth) win[atomicAdd(count, 1)] = comp[i];
+    __syncthreads();
+    nw = *count;
+  }
+  int P2 = 1;
+  while (P2 < nw) P2 <<= 1;
+  for (int i = nw + tid; i < P2; i += blockDim.x) win[i] = ~0ull;
+  __syncthreads();
+  for (int size = 2; size <= P2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = tid; i < P2 / 2; i += blockDim.x) {
+        const int lo = 2 * i - (i & (stride - 1));
+        const int hi = lo + stride;
+        const bool asc = (lo & size) == 0;
+        const uint64_t a = win[lo], b = win[hi];
+        if ((a > b) == asc) {
+          win[lo] = b;
+          win[hi] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int r = tid; r < k; r += blockDim.x) {
+    const size_t o = (size_t)q * k + r;
+    const uint64_t w = r < nw ? win[r] : ~0ull;
+    if (w == ~0ull) {
+      D[o] = IS_IP ? -INFINITY : INFINITY;
+      I[o] = -1;
+      if (P) P[o] = -1;
+    } else {
+      const uint32_t ps = static_cast<uint32_t>(w);
+      D[o] = key_dist(static_cast<uint32_t>(w >> 32), IS_IP);
+      I[o] = ids[ps];
+      if (P) P[o] = ps;
+    }
+  }
+  __syncthreads();
+}
+
 // Exact fallback, on the device: CTA b takes failed queries b, b+grid, ...;
 // exact composites of every row into its scratch slot, block radix select of
 // the k-th, bitonic sort of the winners.  Launched after every MODE 4 merge
@@ -521,55 +581,84 @@ __global__ void __launch_bounds__(256) fallback_kernel(const int* __restrict__ f
       }
       comp[r] = (static_cast<uint64_t>(dist_key(v, IS_IP)) << 32) | static_cast<uint32_t>(r);
     }
-    if (tid == 0) count = 0;
-    __syncthreads();
-    const int nn = (int)n;
-    int nw;
-    if (nn <= k) {
-      for (int i = tid; i < nn; i += blockDim.x) win[i] = comp[i];
-      nw = nn;
-    } else {
-      const uint64_t kth = block_kth([&](int e) { return comp[e]; }, nn, (uint32_t)k, hist, sel);
-      for (int i = tid; i < nn; i += blockDim.x)
-        if (comp[i] <= kth) win[atomicAdd(&count, 1)] = comp[i];
-      __syncthreads();
-      nw = count;
-    }
-    int P2 = 1;
-    while (P2 < nw) P2 <<= 1;
-    for (int i = nw + tid; i < P2; i += blockDim.x) win[i] = ~0ull;
-    __syncthreads();
-    for (int size = 2; size <= P2; size <<= 1) {
-      for (int stride = size >> 1; stride > 0; stride >>= 1) {
-        for (int i = tid; i < P2 / 2; i += blockDim.x) {
-          const int lo = 2 * i - (i & (stride - 1));
-          const int hi = lo + stride;
-          const bool asc = (lo & size) == 0;
-          const uint64_t a = win[lo], b = win[hi];
-          if ((a > b) == asc) {
-            win[lo] = b;
-            win[hi] = a;
-          }
-        }
-        __syncthreads();
-      }
-    }
-    for (int r = tid; r < k; r += blockDim.x) {
-      const size_t o = (size_t)q * k + r;
-      const uint64_t w = r < nw ? win[r] : ~0ull;
-      if (w == ~0ull) {
-        D[o] = IS_IP ? -INFINITY : INFINITY;
-        I[o] = -1;
-        if (P) P[o] = -1;
-      } else {
-        const uint32_t ps = static_cast<uint32_t>(w);
-        D[o] = key_dist(static_cast<uint32_t>(w >> 32), IS_IP);
-        I[o] = ids[ps];
-        if (P) P[o] = ps;
-      }
-    }
+    block_select_write<IS_IP>(comp, (int)n, k, q, win, &count, hist, sel, ids, D, I, P);
     __syncthreads();
   }
+}
+
+// ------------------------------------------------------------ direct path (nq < blas_threshold)
+// Reference flat.py:58-62 sends batches below config.blas_threshold (20,
+// config.py:9) to flat_search (flat.py:76-91): per-pair DIRECT distances
+// (pairwise -> dist_one, _ckernels.pyx:49-57: L2 sum (q - x)^2, IP sum q x)
+// ranked by topk_rows.  Here: one warp per stored row evaluates every query
+// of the group, accumulating in fp64 from the stored operands (fp32: hi + lo
+// == x exactly; fold: -2x scaled back) and rounding once to fp32 -- a self
+// distance is exactly +0.0 -- then one CTA per query selects the top-k.
+template <int MODE>
+__device__ __forceinline__ double stored_val(const void* a, const void* b, size_t off) {
+  if (MODE == 0) return (double)(static_cast<const float*>(a)[off] + static_cast<const float*>(b)[off]);
+  if (MODE == 4) return (double)static_cast<const float*>(a)[off];
+  if (MODE == 1) return (double)__half2float(static_cast<const __half*>(a)[off]);
+  return (double)__bfloat162float(static_cast<const __nv_bfloat16*>(a)[off]);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) direct_dist_kernel(const void* __restrict__ q0, const void* __restrict__ q1,
+                                                          int nq, const void* __restrict__ s0,
+                                                          const void* __restrict__ s1, int64_t n, int d, int dp,
+                                                          int is_ip, int fold, uint64_t* __restrict__ comp) {
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= n) return;
+  constexpr int XR = 8;  // stored row cached in registers for d <= 256
+  double xv[XR];
+#pragma unroll
+  for (int i = 0; i < XR; ++i) {
+    const int c = lane + 32 * i;
+    xv[i] = c < d ? stored_val<MODE>(s0, s1, (size_t)r * dp + c) * (fold ? -0.5 : 1.0) : 0.0;  // -2x folded (exact)
+  }
+  for (int qi = 0; qi < nq; ++qi) {
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < XR; ++i) {
+      const int c = lane + 32 * i;
+      if (c < d) {
+        const double qv = stored_val<MODE>(q0, q1, (size_t)qi * dp + c);
+        if (is_ip) acc = fma(qv, xv[i], acc);
+        else {
+          const double t = qv - xv[i];
+          acc = fma(t, t, acc);
+        }
+      }
+    }
+    for (int c = lane + 32 * XR; c < d; c += 32) {
+      const double qv = stored_val<MODE>(q0, q1, (size_t)qi * dp + c);
+      const double x = stored_val<MODE>(s0, s1, (size_t)r * dp + c) * (fold ? -0.5 : 1.0);
+      if (is_ip) acc = fma(qv, x, acc);
+      else {
+        const double t = qv - x;
+        acc = fma(t, t, acc);
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(FULLMASK, acc, off);
+    if (lane == 0) {
+      const float v = static_cast<float>(acc);
+      comp[(size_t)qi * n + r] = (static_cast<uint64_t>(dist_key(v, is_ip != 0)) << 32) | static_cast<uint32_t>(r);
+    }
+  }
+}
+
+template <bool IS_IP>
+__global__ void __launch_bounds__(256) direct_select_kernel(const uint64_t* __restrict__ comp, int64_t n, int q0,
+                                                            int k, const int64_t* __restrict__ ids,
+                                                            float* __restrict__ D, int64_t* __restrict__ I,
+                                                            int64_t* __restrict__ P) {
+  extern __shared__ uint64_t win[];
+  __shared__ int count;
+  __shared__ uint32_t hist[256], sel[8];
+  block_select_write<IS_IP>(comp + (size_t)blockIdx.x * n, (int)n, k, q0 + blockIdx.x, win, &count, hist, sel, ids,
+                            D, I, P);
 }
 
 // ------------------------------------------------------------ conversions
@@ -630,10 +719,11 @@ __global__ void prep_rows_kernel(const void* __restrict__ x, int in_dtype, int64
   if (lane == 0 && norms != nullptr) norms[orow] = xn;
   if (MODE == 2 && fold && lane < 3) {
     // xn = h0 + h1 + h2 exactly: each bf16 takes the next 8 significant bits
+    // (a non-finite norm goes whole into h0: inf - inf would make h1 NaN)
     float part = xn, hv = 0.f;
     for (int i = 0; i <= lane; ++i) {
       hv = __bfloat162float(__float2bfloat16_rn(part));
-      part -= hv;  // exact (Sterbenz / representable remainder)
+      part = isfinite(part) ? part - hv : 0.f;  // exact (Sterbenz / representable remainder)
     }
     static_cast<__nv_bfloat16*>(out0)[(size_t)orow * dp + d + lane] = __float2bfloat16_rn(fold == 1 ? hv : 1.f);
   }

@@ -676,8 +676,11 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       const float band4 = (MODE == 4 && KQ > 0 && !RANGE && row_ok)
                               ? (tf32_exact ? 0.f : (IS_IP ? 0.0078125f : 0.015625f)) *
                                         sqrtf(fmaxf(p.qnorm[row], 0.f) * fmaxf(*p.xn_max, 0.f)) +
-                                    // exact products: only the two fp32 accumulation orders differ
-                                    (float)dp * 1.1920928955078125e-07f *
+                                    // fp32 accumulation: the tensor core (possibly truncating,
+                                    // <= dp 2^-23) and the sequential-FMA rescoring (<= dp 2^-24)
+                                    // each err by <= dp u (qn + max xn); band = 2e, 2x safety,
+                                    // + the final (qn + xn) - 2ip roundings
+                                    (4.f * (float)dp + 8.f) * 1.1920928955078125e-07f *
                                         (fmaxf(p.qnorm[row], 0.f) + fmaxf(*p.xn_max, 0.f))
                               : 0.f;
       uint32_t min_lost = 0xFFFFFFFFu;  // MODE 4: smallest key dropped from a full queue

@@ -2,13 +2,15 @@
 
 Every search runs the sm_100a path through the C ABI (``include/flatknn.h``):
 query prep kernel -> fused tcgen05 GEMM + top-k kernel -> merge kernel.
-There is no CPU fallback and no nq-threshold dispatch: the reference's
-``nq < config.blas_threshold`` direct path (flat.py:58-62) exists only to
-avoid BLAS overhead on a CPU, and both of its paths compute the same exact
-top-k under the same (distance, position) order.
+There is no CPU fallback.  The reference's ``nq < config.blas_threshold``
+dispatch (flat.py:58-62) is kept: small batches take a GPU direct path
+(exact per-pair distances, flat.py:76-91), so e.g. a self-distance is
+exactly 0.0 as test_flat.py:37-43 asserts.
 
 Storage modes:
-  "fp32" -- fp32 vectors searched with a 3xTF32 split (fp32-faithful);
+  "fp32" -- fp32 vectors (stored as an exact tf32 hi/lo split), searched with
+  one tf32 tensor-core pass + certified exact fp32 rescoring (k <= 16 over
+  >= 256k rows) or 3xTF32 -- fp32-faithful either way;
   "fp16" / "bf16" -- vectors (and queries) rounded RNE to 16 bits, single
   tensor-core pass; norms are computed from the rounded values, so results
   equal the reference run on the same rounded inputs.
@@ -21,6 +23,7 @@ import ctypes
 import numpy as np
 
 from . import _native as N
+from . import config
 from .core import (METRIC_IP, METRIC_L2, Index, Metric, RangeResult, SearchResult, as_vectors, is_torch,
                    metric_value)
 
@@ -75,6 +78,7 @@ class FlatIndex(Index):
         N.check(L.fk_create(self.device, self.d, self._mcode, _STORAGE[storage], ctypes.byref(h)))
         self._h = h
         self._pos_of_id: dict[int, int] | None = None
+        self._blas_threshold = 20  # the native default (config.py:9)
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -160,9 +164,16 @@ class FlatIndex(Index):
 
     # ------------------------------------------------------------------ search
     def _search(self, q, k: int, with_positions: bool = False):
-        """flat.py:58-62 / 94-118 on the GPU; returns SearchResult (+ positions)."""
+        """flat.py:58-62 on the GPU: batches of >= ``config.blas_threshold``
+        queries run the fused GEMM + top-k path (flat_search_blas, 94-118),
+        smaller ones the direct per-pair path (flat_search, 76-91).  Returns
+        SearchResult (+ storage positions)."""
         nq = q.shape[0]
         L = N.lib()
+        bt = int(config.blas_threshold)
+        if bt != self._blas_threshold:
+            N.check(L.fk_set_option(self._h, N.FK_OPT_BLAS_THRESHOLD, bt))
+            self._blas_threshold = bt
         if is_torch(q) and q.is_cuda:
             if q.device.index != self.device:
                 q = q.to(f"cuda:{self.device}")
@@ -185,29 +196,42 @@ class FlatIndex(Index):
 
     def _range_search(self, q, radius: float) -> RangeResult:
         """flat.py:121-144 on the GPU: direct distances (<= radius; >= for
-        IP), each query's list best first, ties by smaller id (flat.py:137)."""
+        IP), each query's list best first, ties by smaller id (flat.py:137).
+        The entries come back in a per-call native result object, so
+        concurrent range searches on one index cannot mix results."""
         nq = q.shape[0]
         L = N.lib()
         total = ctypes.c_int64(0)
-        if is_torch(q) and q.is_cuda:
-            if q.device.index != self.device:
-                q = q.to(f"cuda:{self.device}")
-            lims = torch.empty(nq + 1, dtype=torch.int64, device=q.device)
-            N.check(L.fk_range_search(self._h, _ptr(q), nq, _dtype_code(q), float(radius), _ptr(lims),
-                                      ctypes.byref(total), 1, _stream_of(self.device)))
-            ids = torch.empty(total.value, dtype=torch.int64, device=q.device)
-            dist = torch.empty(total.value, dtype=torch.float32, device=q.device)
-            N.check(L.fk_range_fetch(self._h, _ptr(ids), _ptr(dist), 1, _stream_of(self.device)))
-        else:
-            if is_torch(q):
-                q = q.contiguous()
-            lims = np.empty(nq + 1, dtype=np.int64)
-            N.check(L.fk_range_search(self._h, _ptr(q), nq, _dtype_code(q), float(radius), lims.ctypes.data,
-                                      ctypes.byref(total), 0, 0))
-            ids = np.empty(total.value, dtype=np.int64)
-            dist = np.empty(total.value, dtype=np.float32)
-            N.check(L.fk_range_fetch(self._h, ids.ctypes.data, dist.ctypes.data, 0, 0))
+        res = ctypes.c_void_p()
+        try:
+            if is_torch(q) and q.is_cuda:
+                if q.device.index != self.device:
+                    q = q.to(f"cuda:{self.device}")
+                stream = _stream_of(self.device)
+                lims = torch.empty(nq + 1, dtype=torch.int64, device=q.device)
+                N.check(L.fk_range_search(self._h, _ptr(q), nq, _dtype_code(q), float(radius), _ptr(lims),
+                                          ctypes.byref(total), ctypes.byref(res), 1, stream))
+                ids = torch.empty(total.value, dtype=torch.int64, device=q.device)
+                dist = torch.empty(total.value, dtype=torch.float32, device=q.device)
+                N.check(L.fk_range_fetch(res, _ptr(ids), _ptr(dist), total.value, 1, stream))
+            else:
+                if is_torch(q):
+                    q = q.contiguous()
+                lims = np.empty(nq + 1, dtype=np.int64)
+                N.check(L.fk_range_search(self._h, _ptr(q), nq, _dtype_code(q), float(radius), lims.ctypes.data,
+                                          ctypes.byref(total), ctypes.byref(res), 0, 0))
+                ids = np.empty(total.value, dtype=np.int64)
+                dist = np.empty(total.value, dtype=np.float32)
+                N.check(L.fk_range_fetch(res, ids.ctypes.data, dist.ctypes.data, total.value, 0, 0))
+        finally:
+            if res.value:
+                L.fk_range_free(res)
         return RangeResult(lims, ids, dist, float(radius))
+
+    def set_plan_rows(self, rows: int) -> None:
+        """Choose the fp32 algorithm as for a database of ``rows`` rows (a
+        shard of a row-sharded index passes the global count; 0 = own)."""
+        N.check(N.lib().fk_set_option(self._h, N.FK_OPT_PLAN_ROWS, int(rows)))
 
     def search_with_positions(self, q, k: int):
         """Search returning (SearchResult, storage positions) -- the sharded

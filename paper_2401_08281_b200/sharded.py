@@ -86,6 +86,7 @@ class ShardedFlatIndex:
         lo, hi = shard_range(n, self.rank, self.world)
         self._add_local(x[lo:hi], self.ntotal + lo, ids=None)
         self.ntotal += n
+        self._sync_plan_rows()
 
     def add_with_ids(self, x, ids) -> None:
         x = as_vectors(x, self.d)
@@ -98,6 +99,7 @@ class ShardedFlatIndex:
         lo, hi = shard_range(n, self.rank, self.world)
         self._add_local(x[lo:hi], self.ntotal + lo, ids=ids[lo:hi])
         self.ntotal += n
+        self._sync_plan_rows()
 
     def add_local_shard(self, x_local, global_offset: int, n_global: int, ids_local=None) -> None:
         """Add this rank's own slice of a global batch of ``n_global`` rows whose
@@ -106,6 +108,7 @@ class ShardedFlatIndex:
         x_local = as_vectors(x_local, self.d)
         self._add_local(x_local, self.ntotal + global_offset, ids=ids_local)
         self.ntotal += int(n_global)
+        self._sync_plan_rows()
 
     def add_shard_rows(self, x_rows, global_row0: int) -> None:
         """Append rows of this rank's shard whose positions in the global batch
@@ -117,6 +120,13 @@ class ShardedFlatIndex:
 
     def finish_global_batch(self, n_global: int) -> None:
         self.ntotal += int(n_global)
+        self._sync_plan_rows()
+
+    def _sync_plan_rows(self) -> None:
+        # every shard runs the algorithm the unsharded search would choose
+        # (e.g. fp32 1-pass vs 3xTF32 is decided on the GLOBAL row count)
+        if hasattr(self.local, "set_plan_rows"):
+            self.local.set_plan_rows(self.ntotal)
 
     def _add_local(self, xs, gpos0: int, ids) -> None:
         m = xs.shape[0]
@@ -132,6 +142,7 @@ class ShardedFlatIndex:
     def reset(self) -> None:
         self.local.reset()
         self.ntotal = 0
+        self._sync_plan_rows()
         self._gpos_parts = []
         self._gpos = None
 
