@@ -17,6 +17,8 @@
  *   (Faiss-style reset; none in ref)   SURVEY 8(b)        fk_reset
  *   FlatIndex.reconstruct_batch        flat.py:43-44      fk_reconstruct
  *   FlatIndex.remove_ids               flat.py:46-56      fk_remove_ids
+ *   FlatIndex._positions (id -> pos)   flat.py:34-41      fk_positions
+ *   refine_search re-ranking           core.py:368-394    fk_refine
  *   _kernels function table errors     _kernels/__init__.py:37-41 -> fk_last_error
  *   (none: SPEC.md:115 non-goal)       SURVEY 8(e)        fk_merge_shards
  *
@@ -46,8 +48,9 @@ typedef struct fk_index fk_index;
 #define FK_METRIC_L2 1
 
 /* storage / input dtypes */
-#define FK_F32 0  /* storage: fp32 (hi/lo tf32 split kept; k <= 16 over >= 256k rows: one tf32
-                     pass + certified exact fp32 rescoring, else 3xTF32; fp32-faithful) */
+#define FK_F32 0  /* storage: fp32 (k <= 16 over >= 256k rows: raw fp32 rows, one tf32 pass
+                     + certified exact fp32 rescoring; otherwise the hi/lo tf32 split and
+                     3xTF32; fp32-faithful either way) */
 #define FK_F16 1  /* storage: fp16 (RNE from f32), tensor-core kind::f16      */
 #define FK_BF16 2 /* storage: bf16 (RNE from f32), tensor-core kind::f16      */
 
@@ -92,8 +95,26 @@ int fk_merge_shards(int metric, int nshard, int64_t nq, int k, const float* D_in
 int fk_reconstruct(fk_index* h, const int64_t* positions, int64_t n, float* out, int on_device, void* stream);
 
 /* Remove every stored vector whose id is in ids[0..n) (flat.py:46-56),
- * compacting storage in place and preserving order.  *removed = count. */
+ * compacting storage in place and preserving order.  *removed = count.
+ * Runs on the device (sorted kill list, keep mask, ordered compaction); only
+ * the removed count comes back to the host. */
 int fk_remove_ids(fk_index* h, const int64_t* ids, int64_t n, int on_device, int64_t* removed, void* stream);
+
+/* ids[0..n) -> storage positions (flat.py:34-41 `_positions`): a duplicated
+ * id maps to its LAST position, as the reference's {id: i} dict does.
+ * FK_E_NOTFOUND (KeyError) names the first unknown id.  The sorted id table
+ * lives on the device and is rebuilt lazily after add / remove / reset. */
+int fk_positions(fk_index* h, const int64_t* ids, int64_t n, int64_t* pos, int on_device, void* stream);
+
+/* refine_search (core.py:368-394) with this index as `exact`: q [nq][d]
+ * float32 queries, cand [nq][L] shortlist ids from the fast index (-1 =
+ * empty, skipped; unknown ids -> FK_E_NOTFOUND like reconstruct_batch).
+ * Each candidate gets the direct distance of its stored vector (fp64
+ * accumulation, one rounding to fp32) under `metric` (the FAST index's,
+ * core.py:375); D/I [nq][k] = the first k by (value best first, id), padded
+ * with -1 and +inf (L2) / -inf (IP).  L <= 14464 (shortlist held in smem). */
+int fk_refine(fk_index* h, int metric, const float* q, int64_t nq, const int64_t* cand, int L, int k, float* D,
+              int64_t* I, int on_device, void* stream);
 
 /* Drop all vectors, keep the device allocation (Faiss Index::reset). */
 int fk_reset(fk_index* h);
@@ -116,6 +137,12 @@ const char* fk_last_error(void);
  * total kernel launches of those searches.  Then it resets the accumulators. */
 int fk_set_profiling(fk_index* h, int on);
 int fk_kernel_times(fk_index* h, float* ms3, int* nlaunch);
+
+/* Timed-loop gate (bench instrumentation, no reference counterpart): enqueue
+ * a one-thread kernel on `stream` that waits until *host_flag (pinned host
+ * memory) is nonzero or timeout_s seconds pass, so a timed loop can enqueue
+ * all its work before the GPU starts and host jitter cannot idle the GPU. */
+int fk_gate(const int* host_flag, double timeout_s, void* stream);
 
 /* Range search (replaces annkit flat.py:121-144 `flat_range_search`, reached
  * through Index.range_search core.py:152-155 / FlatIndex._range_search):

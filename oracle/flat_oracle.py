@@ -22,6 +22,11 @@ It restates, in plain numpy, the reference annkit BLAS search path
                            config.blas_threshold, flat.py:58-62) with pairwise
                            -> dist_one (``_ckernels.pyx:49-57``): L2 sum (q-x)^2,
                            IP sum q x, here accumulated in fp64 and rounded once
+* ``refine_rerank``     <- ``pkg/src/annkit/core.py:368-394`` (refine_search's
+                           re-ranking of a given shortlist: reconstruct from
+                           the exact index, direct distances, (value, id) order)
+* ``remove_ids``        <- ``pkg/src/annkit/flat.py:46-56`` (isin mask, order kept)
+* ``positions``         <- ``pkg/src/annkit/flat.py:34-41`` ({id: pos}: last wins)
 * ``merge_topk``        <- the total order of ``core.py:205-236`` (64-bit key
                            ``monotone(value) << 32 | column``) applied to the
                            union of per-shard top-k lists carrying GLOBAL
@@ -274,3 +279,43 @@ def flat_range_search(xb: np.ndarray, q: np.ndarray, radius: float, metric: str 
     cat_i = np.concatenate(out_i) if out_i else np.empty(0, np.int64)
     cat_d = np.concatenate(out_d) if out_d else np.empty(0, np.float32)
     return lims, cat_i, cat_d.astype(np.float32)
+
+
+def positions(ids_table: np.ndarray, ids) -> np.ndarray:
+    """flat.py:34-41: id -> position through ``{int(v): i for i, v in
+    enumerate(ids)}`` (a repeated id maps to its LAST position); KeyError."""
+    pos_of = {int(v): i for i, v in enumerate(ids_table)}
+    try:
+        return np.array([pos_of[int(v)] for v in np.atleast_1d(ids)], dtype=np.int64)
+    except KeyError as exc:
+        raise KeyError(f"unknown id {exc.args[0]}") from None
+
+
+def remove_ids(xb: np.ndarray, ids_table: np.ndarray, kill):
+    """flat.py:46-56: drop every row whose id is in ``kill``, keep order.
+    Returns (vectors, ids, removed)."""
+    mask = np.isin(ids_table, np.asarray(kill, dtype=np.int64))
+    return xb[~mask], ids_table[~mask], int(mask.sum())
+
+
+def refine_rerank(xb: np.ndarray, ids_table: np.ndarray, q: np.ndarray, cand: np.ndarray, k: int,
+                  metric: str = METRIC_L2):
+    """core.py:368-394 given the fast index's shortlist ``cand`` (nq, L):
+    per query drop -1, reconstruct the candidates from the exact index
+    (flat.py:43-44), direct distances (pairwise_distances), keep the first k
+    by (value best first, id) with Python's stable sort, pad -1 / +-inf."""
+    nq = q.shape[0]
+    desc = metric == METRIC_IP
+    out_ids = np.full((nq, k), -1, dtype=np.int64)
+    out_dist = np.full((nq, k), -np.inf if desc else np.inf, dtype=np.float32)
+    for i in range(nq):
+        c = cand[i][cand[i] >= 0]
+        if len(c) == 0:
+            continue
+        vecs = xb[positions(ids_table, c)]
+        dists = direct_distances(q[i:i + 1], vecs, metric)[0]
+        order = sorted(range(len(c)), key=lambda j: (-dists[j] if desc else dists[j], c[j]))[:k]
+        for slot, j in enumerate(order):
+            out_ids[i, slot] = c[j]
+            out_dist[i, slot] = dists[j]
+    return out_ids, out_dist

@@ -10,7 +10,7 @@ top-k) behind the C ABI declared in ``include/flatknn.h``.
 from . import config
 from .core import (METRIC_IP, METRIC_L2, Index, Metric, MetricKind, RangeResult, SearchResult, as_vectors,
                    knn_recall)
-from .flat import FlatIndex, IndexFlatIP, IndexFlatL2
+from .flat import FlatIndex, IndexFlatIP, IndexFlatL2, refine_search
 from .kmeans import assign_vectors, coarse_quantizer, kmeans_assign, probe_lists
 from .sharded import ShardedFlatIndex
 
@@ -35,4 +35,5 @@ __all__ = [
     "kmeans_assign",
     "knn_recall",
     "probe_lists",
+    "refine_search",
 ]

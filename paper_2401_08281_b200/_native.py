@@ -29,6 +29,7 @@ EXPORTED = (
     "fk_reset", "fk_ntotal", "fk_dim", "fk_get_ids", "fk_destroy", "fk_last_error",
     "fk_set_profiling", "fk_kernel_times", "fk_last_plan", "fk_kmeans_rescore",
     "fk_range_search", "fk_range_fetch", "fk_range_total", "fk_range_free", "fk_set_option",
+    "fk_positions", "fk_refine", "fk_gate",
 )
 
 FK_OPT_PLAN_ROWS = 1
@@ -62,6 +63,9 @@ _SIGS = {
     "fk_range_total": (_I64, [_P]),
     "fk_range_free": (None, [_P]),
     "fk_set_option": (_INT, [_P, _INT, _I64]),
+    "fk_gate": (_INT, [_P, ctypes.c_double, _P]),
+    "fk_positions": (_INT, [_P, _P, _I64, _P, _INT, _P]),
+    "fk_refine": (_INT, [_P, _INT, _P, _I64, _P, _INT, _INT, _P, _P, _INT, _P]),
     "fk_kmeans_rescore": (_INT, [_P, _I64, _INT, _P, _P, _I64, _P, _INT, _INT, _P, ctypes.c_double,
                                  ctypes.c_double, _P, _P, _P, _P]),
     "fk_debug_set_ip_dump": (_INT, [_P, _P]),

@@ -21,10 +21,12 @@
 
 #include "fk_host.cuh"
 #include "flatknn_kernels.cuh"
+#include "storage_kernels.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 
 using namespace fk;
 using fkh::set_err;
@@ -139,6 +141,10 @@ struct fk_index {
   // every call that touches the handle's scratch or storage waits for the
   // previous such call's stream work (stream-ordered reuse: concurrent
   // searches on different streams stay correct) and records this event
+  // sorted (id, position) table for id -> position lookups (flat.py:34-41),
+  // rebuilt lazily after add / remove / reset
+  DevBuf idt_keys, idt_pos, idt_tmp, idt_miss, rm_kill, rm_flags, rm_keep;
+  int64_t idt_n = -1;
   cudaEvent_t scratch_ev = nullptr;
   bool scratch_used = false;
   int64_t plan_rows = 0;  // FK_OPT_PLAN_ROWS (0: ntotal)
@@ -373,7 +379,8 @@ void fk_destroy(fk_index* h) {
   for (DevBuf* b : {&h->q_in, &h->q0, &h->q1, &h->qn, &h->pkey, &h->ppos, &h->thr, &h->pcnt, &h->cbuf, &h->fail,
                     &h->outD, &h->outI, &h->outP, &h->stage_in, &h->stage_ids, &h->rfail, &h->rcomp, &h->rflag,
                     &h->glock, &h->gkeys, &h->rcand, &h->rcount, &h->rdist, &h->rkid, &h->rkrd, &h->rkeep,
-                    &h->rrowc, &h->rsel, &h->rnsel, &h->rtmp, &h->rkid2, &h->rkrd2, &h->rv1, &h->rv2, &h->rlims})
+                    &h->rrowc, &h->rsel, &h->rnsel, &h->rtmp, &h->rkid2, &h->rkrd2, &h->rv1, &h->rv2, &h->rlims,
+                    &h->idt_keys, &h->idt_pos, &h->idt_tmp, &h->idt_miss, &h->rm_kill, &h->rm_flags, &h->rm_keep})
     b->release();
   if (h->scratch_ev) cudaEventDestroy(h->scratch_ev);
   cudaFree(h->xn_max);
@@ -393,6 +400,7 @@ int fk_reset(fk_index* h) {
   CK(cudaMemset(h->xn_max, 0, sizeof(float)));
   CK(cudaMemset(h->inexact, 0, 2 * sizeof(unsigned int)));
   h->ntotal = 0;
+  h->idt_n = -1;
   return FK_OK;
 }
 
@@ -440,6 +448,7 @@ int fk_add(fk_index* h, const void* x, int64_t n, int dtype, const int64_t* ids,
   if ((rc = scratch_end(h, st))) return rc;
   if (!on_device) CK(cudaStreamSynchronize(st));
   h->ntotal += n;
+  h->idt_n = -1;
   return FK_OK;
 }
 
@@ -1280,43 +1289,218 @@ int fk_remove_ids(fk_index* h, const int64_t* ids, int64_t n, int on_device, int
   std::lock_guard<std::mutex> g(h->mu);
   CK(cudaSetDevice(h->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  std::vector<int64_t> del(n), cur(h->ntotal);
-  CK(cudaMemcpyAsync(del.data(), ids, n * sizeof(int64_t), on_device ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost,
+  int rc = scratch_begin(h, st);
+  if (rc) return rc;
+  const int64_t nt = h->ntotal;
+  // kill list -> device, sorted (np.isin, flat.py:47)
+  if ((rc = h->rm_kill.ensure((size_t)n * 16))) return rc;
+  int64_t* kill = static_cast<int64_t*>(h->rm_kill.p);
+  int64_t* kill_sorted = kill + n;
+  CK(cudaMemcpyAsync(kill, ids, n * sizeof(int64_t), on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                      st));
-  CK(cudaMemcpyAsync(cur.data(), h->ids, h->ntotal * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  size_t tb_sort = 0, tb_sel = 0;
+  CK(cub::DeviceRadixSort::SortKeys(nullptr, tb_sort, kill, kill_sorted, n, 0, 64, st));
+  CK(cub::DeviceSelect::Flagged(nullptr, tb_sel, cub::CountingInputIterator<int64_t>(0), (const uint8_t*)nullptr,
+                                (int64_t*)nullptr, (int64_t*)nullptr, nt, st));
+  if ((rc = h->idt_tmp.ensure(std::max(tb_sort, tb_sel)))) return rc;
+  CK(cub::DeviceRadixSort::SortKeys(h->idt_tmp.p, tb_sort, kill, kill_sorted, n, 0, 64, st));
+  // keep mask over storage, then the ordered keep list (flat.py:49-53)
+  if ((rc = h->rm_flags.ensure((size_t)nt + 16))) return rc;
+  if ((rc = h->rm_keep.ensure((size_t)(nt + 1) * sizeof(int64_t)))) return rc;
+  auto flags = static_cast<uint8_t*>(h->rm_flags.p);
+  auto keep = static_cast<int64_t*>(h->rm_keep.p);
+  int64_t* nsel = keep + nt;
+  keep_flags_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(h->ids, nt, kill_sorted, n, flags);
+  CKL();
+  CK(cub::DeviceSelect::Flagged(h->idt_tmp.p, tb_sel, cub::CountingInputIterator<int64_t>(0), flags, keep, nsel, nt,
+                                st));
+  int64_t nk = 0;
+  CK(cudaMemcpyAsync(&nk, nsel, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  std::unordered_set<int64_t> kill(del.begin(), del.end());
-  std::vector<int64_t> keep;
-  keep.reserve(h->ntotal);
-  for (int64_t i = 0; i < h->ntotal; ++i)
-    if (!kill.count(cur[i])) keep.push_back(i);
-  const int64_t nrem = h->ntotal - (int64_t)keep.size();
+  const int64_t nrem = nt - nk;
   if (removed) *removed = nrem;
-  if (nrem == 0) return FK_OK;
-  const int64_t nk = (int64_t)keep.size();
-  int rc;
-  if (nk > 0) {
-    if ((rc = h->stage_ids.ensure(nk * sizeof(int64_t)))) return rc;
-    CK(cudaMemcpyAsync(h->stage_ids.p, keep.data(), nk * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-    const int64_t* dkeep = static_cast<const int64_t*>(h->stage_ids.p);
+  if (nrem > 0 && nk > 0) {
+    // compact every column in place, order preserved: keep[i] >= i, so a
+    // slice [c0, c0 + m) gathered through scratch only reads rows >= c0
+    // that later slices have not overwritten yet
     const size_t rb = row_bytes(h);
-    // compact every column of the store through a scratch buffer (order preserved, flat.py:50-53)
     struct Col {
       void* p;
       size_t rb;
     } cols[4] = {{h->s0, rb}, {h->s1, rb}, {h->norms, sizeof(float)}, {h->ids, sizeof(int64_t)}};
+    const int64_t slice = std::max<int64_t>(1, (int64_t)((256ull << 20) / rb));
+    if ((rc = h->stage_in.ensure((size_t)std::min(slice, nk) * rb))) return rc;
     for (auto& c : cols) {
       if (!c.p) continue;
-      if ((rc = h->stage_in.ensure(nk * c.rb))) return rc;
-      gather_rows_kernel<<<(unsigned)nk, 128, 0, st>>>(static_cast<const uint8_t*>(c.p),
-                                                        static_cast<uint8_t*>(h->stage_in.p), c.rb, dkeep, nk);
-      CKL();
-      CK(cudaMemcpyAsync(c.p, h->stage_in.p, nk * c.rb, cudaMemcpyDeviceToDevice, st));
+      const int64_t cs = std::max<int64_t>(1, (int64_t)((256ull << 20) / c.rb));
+      for (int64_t c0 = 0; c0 < nk; c0 += cs) {
+        const int64_t m = std::min(cs, nk - c0);
+        gather_rows_kernel<<<(unsigned)m, 128, 0, st>>>(static_cast<const uint8_t*>(c.p),
+                                                         static_cast<uint8_t*>(h->stage_in.p), c.rb, keep + c0, m);
+        CKL();
+        CK(cudaMemcpyAsync(static_cast<uint8_t*>(c.p) + (size_t)c0 * c.rb, h->stage_in.p, m * c.rb,
+                           cudaMemcpyDeviceToDevice, st));
+      }
     }
+  }
+  if (nrem > 0) {
+    // the filter bound needs max stored norm: recompute over the survivors
+    CK(cudaMemsetAsync(h->xn_max, 0, sizeof(float), st));
+    if (nk > 0) {
+      norm_max_kernel<<<(unsigned)std::min<int64_t>((nk + 255) / 256, 1024), 256, 0, st>>>(
+          h->norms, nk, reinterpret_cast<unsigned int*>(h->xn_max));
+      CKL();
+    }
+    h->ntotal = nk;
+    h->idt_n = -1;
+  }
+  if ((rc = scratch_end(h, st))) return rc;
+  CK(cudaStreamSynchronize(st));
+  return FK_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Build (lazily) the stably sorted (id, position) table.
+int ensure_id_table(fk_index* h, cudaStream_t st) {
+  const int64_t n = h->ntotal;
+  if (h->idt_n == n) return FK_OK;
+  int rc;
+  if ((rc = h->idt_keys.ensure((size_t)n * 8))) return rc;
+  if ((rc = h->idt_pos.ensure((size_t)n * 16))) return rc;
+  auto keys = static_cast<int64_t*>(h->idt_keys.p);
+  auto pos = static_cast<int64_t*>(h->idt_pos.p);
+  int64_t* iota = pos + n;
+  iota_ids_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(iota, 0, n);
+  CKL();
+  size_t tb = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, h->ids, keys, iota, pos, n, 0, 64, st));
+  if ((rc = h->idt_tmp.ensure(tb))) return rc;
+  CK(cub::DeviceRadixSort::SortPairs(h->idt_tmp.p, tb, h->ids, keys, iota, pos, n, 0, 64, st));
+  h->idt_n = n;
+  return FK_OK;
+}
+
+// ids [m] (device) -> positions [m] (device); FK_E_NOTFOUND naming the first
+// unknown id.  Caller holds the lock and has ordered the stream.
+int lookup_positions(fk_index* h, const int64_t* ids, int64_t m, int skip_negative, int64_t* pos, cudaStream_t st) {
+  int rc;
+  if ((rc = ensure_id_table(h, st))) return rc;
+  if ((rc = h->idt_miss.ensure(sizeof(unsigned long long)))) return rc;
+  auto miss = static_cast<unsigned long long*>(h->idt_miss.p);
+  CK(cudaMemsetAsync(miss, 0xFF, sizeof(unsigned long long), st));
+  lookup_positions_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(
+      static_cast<const int64_t*>(h->idt_keys.p), static_cast<const int64_t*>(h->idt_pos.p), h->ntotal, ids, m,
+      skip_negative, pos, miss);
+  CKL();
+  unsigned long long first = 0;
+  CK(cudaMemcpyAsync(&first, miss, sizeof first, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (first != ~0ull) {
+    int64_t bad = 0;
+    CK(cudaMemcpy(&bad, ids + first, sizeof bad, cudaMemcpyDeviceToHost));
+    return set_err(FK_E_NOTFOUND, "unknown id %lld", (long long)bad);
+  }
+  return FK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fk_positions(fk_index* h, const int64_t* ids, int64_t n, int64_t* pos, int on_device, void* stream) {
+  if (!h) return set_err(FK_E_INVALID, "NULL index");
+  if (n <= 0) return FK_OK;
+  if (!ids || !pos) return set_err(FK_E_INVALID, "NULL argument");
+  std::lock_guard<std::mutex> g(h->mu);
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int rc = scratch_begin(h, st);
+  if (rc) return rc;
+  const int64_t* dids = ids;
+  int64_t* dpos = pos;
+  if (!on_device) {
+    if ((rc = h->stage_ids.ensure((size_t)n * 16))) return rc;
+    auto sp = static_cast<int64_t*>(h->stage_ids.p);
+    CK(cudaMemcpyAsync(sp, ids, n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    dids = sp;
+    dpos = sp + n;
+  }
+  rc = lookup_positions(h, dids, n, 0, dpos, st);
+  if (rc == FK_OK && !on_device) {
+    CK(cudaMemcpyAsync(pos, dpos, n * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
   }
-  h->ntotal = nk;
-  return FK_OK;
+  const int rc2 = scratch_end(h, st);
+  return rc ? rc : rc2;
+}
+
+int fk_refine(fk_index* h, int metric, const float* q, int64_t nq, const int64_t* cand, int L, int k, float* D,
+              int64_t* I, int on_device, void* stream) {
+  if (!h) return set_err(FK_E_INVALID, "NULL index");
+  if (k < 1) return set_err(FK_E_INVALID, "k must be >= 1");
+  if (L < k) return set_err(FK_E_INVALID, "shortlist must be >= k");
+  if (metric != FK_METRIC_L2 && metric != FK_METRIC_IP) return set_err(FK_E_UNSUPPORTED, "metric %d", metric);
+  if (nq <= 0) return FK_OK;
+  if (!q || !cand || !D || !I) return set_err(FK_E_INVALID, "NULL argument");
+  const size_t smem = (size_t)L * 16;
+  if (smem > (size_t)SMEM_LIMIT) return set_err(FK_E_UNSUPPORTED, "shortlist %d above %d", L, SMEM_LIMIT / 16);
+  std::lock_guard<std::mutex> g(h->mu);
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int rc = scratch_begin(h, st);
+  if (rc) return rc;
+  const size_t nc = (size_t)nq * L;
+  const float* dq = q;
+  const int64_t* dc = cand;
+  float* dD = D;
+  int64_t* dI = I;
+  if (!on_device) {
+    if ((rc = h->stage_in.ensure((size_t)nq * h->d * 4 + (size_t)nq * k * 4))) return rc;
+    if ((rc = h->rkeep.ensure(nc * 8 + (size_t)nq * k * 8))) return rc;
+    auto sq = static_cast<float*>(h->stage_in.p);
+    auto sc = static_cast<int64_t*>(h->rkeep.p);
+    CK(cudaMemcpyAsync(sq, q, (size_t)nq * h->d * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(sc, cand, nc * 8, cudaMemcpyHostToDevice, st));
+    dq = sq;
+    dc = sc;
+    dD = sq + (size_t)nq * h->d;
+    dI = sc + nc;
+  }
+  if ((rc = h->stage_ids.ensure(nc * 8))) return rc;
+  auto cpos = static_cast<int64_t*>(h->stage_ids.p);
+  if ((rc = lookup_positions(h, dc, (int64_t)nc, 1, cpos, st))) {
+    scratch_end(h, st);
+    return rc;
+  }
+  static std::atomic<uint64_t> cfg[5];
+  const int mode = h->storage == FK_F32 ? (h->split == 2 ? 0 : 4) : (h->storage == FK_F16 ? 1 : 2);
+  const double scale = h->fold ? -0.5 : 1.0;
+  const int ip = metric == FK_METRIC_IP;
+#define FK_REFINE(M)                                                                                       \
+  do {                                                                                                     \
+    if ((rc = fkh::once_per_device(cfg[M], [] {                                                            \
+           CK(cudaFuncSetAttribute(refine_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT)); \
+           return FK_OK;                                                                                   \
+         })))                                                                                              \
+      return rc;                                                                                           \
+    refine_kernel<M><<<(unsigned)nq, 256, smem, st>>>(dq, h->d, dc, cpos, L, k, h->s0, h->s1, h->dp, scale, ip, \
+                                                      dD, dI);                                             \
+  } while (0)
+  if (mode == 0) FK_REFINE(0);
+  else if (mode == 4) FK_REFINE(4);
+  else if (mode == 1) FK_REFINE(1);
+  else FK_REFINE(2);
+#undef FK_REFINE
+  CKL();
+  if (!on_device) {
+    CK(cudaMemcpyAsync(D, dD, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(I, dI, (size_t)nq * k * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  return scratch_end(h, st);
 }
 
 int fk_set_profiling(fk_index* h, int on) {
@@ -1334,6 +1518,25 @@ int fk_set_profiling(fk_index* h, int on) {
     }
   }
   h->profiling = on > 0;
+  return FK_OK;
+}
+
+// Device-side gate for timed loops: one thread spins until *flag (pinned
+// host memory, read through UVA) becomes nonzero or timeout_s passes.
+__global__ void gate_kernel(const volatile int* flag, unsigned long long timeout_ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (*flag == 0) {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > timeout_ns) break;
+    __nanosleep(1000);
+  }
+}
+
+int fk_gate(const int* host_flag, double timeout_s, void* stream) {
+  if (!host_flag) return set_err(FK_E_INVALID, "NULL flag");
+  gate_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(host_flag, (unsigned long long)(timeout_s * 1e9));
+  CKL();
   return FK_OK;
 }
 

@@ -77,7 +77,6 @@ class FlatIndex(Index):
         h = ctypes.c_void_p()
         N.check(L.fk_create(self.device, self.d, self._mcode, _STORAGE[storage], ctypes.byref(h)))
         self._h = h
-        self._pos_of_id: dict[int, int] | None = None
         self._blas_threshold = 20  # the native default (config.py:9)
 
     def __del__(self):
@@ -110,13 +109,11 @@ class FlatIndex(Index):
             ids_arg = _ptr(keep)
         stream = _stream_of(self.device) if dev else 0
         N.check(N.lib().fk_add(self._h, _ptr(x), x.shape[0], _dtype_code(x), ids_arg, int(dev), stream))
-        self._pos_of_id = None
 
     def reset(self) -> None:
         """Drop every vector (Faiss ``Index::reset``; not in the reference)."""
         N.check(N.lib().fk_reset(self._h))
         self.ntotal = 0
-        self._pos_of_id = None
 
     @property
     def ids(self) -> np.ndarray:
@@ -132,14 +129,22 @@ class FlatIndex(Index):
         pos = np.arange(self.ntotal, dtype=np.int64)
         return self._reconstruct_positions(pos)
 
+    def _positions_dev(self, ids):
+        """flat.py:34-41 on the device: id -> storage position through the
+        sorted id table (a duplicated id maps to its last position, like the
+        reference's dict); KeyError on unknown ids.  Returns a CUDA tensor."""
+        dev = f"cuda:{self.device}"
+        t = ids if is_torch(ids) else torch.from_numpy(np.ascontiguousarray(np.atleast_1d(np.asarray(ids)),
+                                                                            dtype=np.int64))
+        t = t.reshape(-1).to(device=dev, dtype=torch.int64).contiguous()
+        pos = torch.empty_like(t)
+        if t.numel():
+            N.check(N.lib().fk_positions(self._h, _ptr(t), t.numel(), _ptr(pos), 1, _stream_of(self.device)))
+        return pos
+
     def _positions(self, ids) -> np.ndarray:
         """flat.py:34-41: id -> storage position, KeyError on unknown ids."""
-        if self._pos_of_id is None:
-            self._pos_of_id = {int(v): i for i, v in enumerate(self.ids)}
-        try:
-            return np.array([self._pos_of_id[int(v)] for v in np.atleast_1d(np.asarray(ids))], dtype=np.int64)
-        except KeyError as exc:
-            raise KeyError(f"unknown id {exc.args[0]}") from None
+        return self._positions_dev(ids).cpu().numpy()
 
     def _reconstruct_positions(self, pos: np.ndarray) -> np.ndarray:
         out = np.empty((len(pos), self.d), dtype=np.float32)
@@ -148,18 +153,31 @@ class FlatIndex(Index):
                                            out.ctypes.data, 0, 0))
         return out
 
-    def reconstruct_batch(self, ids) -> np.ndarray:
-        """flat.py:43-44 (exact: fp32 storage keeps hi+lo == x)."""
-        return self._reconstruct_positions(self._positions(ids))
+    def reconstruct_batch(self, ids):
+        """flat.py:43-44 (exact: fp32 storage keeps hi+lo == x).  CUDA ids
+        give a CUDA tensor; anything else a numpy array.  The id lookup and
+        the gather both run on the device."""
+        pos = self._positions_dev(ids)
+        out = torch.empty((pos.numel(), self.d), dtype=torch.float32, device=pos.device)
+        if pos.numel():
+            N.check(N.lib().fk_reconstruct(self._h, _ptr(pos), pos.numel(), _ptr(out), 1,
+                                           _stream_of(self.device)))
+        return out if (is_torch(ids) and ids.is_cuda) else out.cpu().numpy()
 
     def remove_ids(self, ids) -> int:
-        """flat.py:46-56: drop matching ids, keep storage order."""
-        arr = np.ascontiguousarray(np.atleast_1d(np.asarray(ids, dtype=np.int64)))
+        """flat.py:46-56: drop matching ids, keep storage order (mask and
+        compaction on the device)."""
         removed = ctypes.c_int64(0)
-        N.check(N.lib().fk_remove_ids(self._h, arr.ctypes.data, arr.size, 0, ctypes.byref(removed), 0))
+        if is_torch(ids) and ids.is_cuda:
+            t = ids.reshape(-1).to(device=f"cuda:{self.device}", dtype=torch.int64).contiguous()
+            N.check(N.lib().fk_remove_ids(self._h, _ptr(t), t.numel(), 1, ctypes.byref(removed),
+                                          _stream_of(self.device)))
+        else:
+            if is_torch(ids):
+                ids = ids.cpu().numpy()
+            arr = np.ascontiguousarray(np.atleast_1d(np.asarray(ids, dtype=np.int64)))
+            N.check(N.lib().fk_remove_ids(self._h, arr.ctypes.data, arr.size, 0, ctypes.byref(removed), 0))
         self.ntotal -= int(removed.value)
-        if removed.value:
-            self._pos_of_id = None
         return int(removed.value)
 
     # ------------------------------------------------------------------ search
@@ -258,6 +276,38 @@ class FlatIndex(Index):
         N.check(N.lib().fk_last_plan(self._h, v))
         keys = ("grid", "S", "chunk_tiles", "units", "stages", "a_mode", "smem", "kq", "acc_stages", "epi", "bn", "kmode")
         return dict(zip(keys, list(v)))
+
+
+def refine_search(fast: Index, exact: FlatIndex, q, k: int, shortlist: int) -> SearchResult:
+    """Two-stage search (reference core.py:368-394): a ``shortlist`` from the
+    fast index, re-ranked with exact distances of the vectors stored in
+    ``exact`` -- on the GPU (``fk_refine``: id lookup, direct fp64-accumulated
+    distance per candidate, (value, id) order, -1 / +-inf padding).  ``fast``
+    is any index with ``search``; ``exact`` must be a GPU ``FlatIndex``.
+    The metric is the fast index's (core.py:375)."""
+    if shortlist < k:
+        raise ValueError("shortlist must be >= k")
+    q = as_vectors(q, fast.d)
+    if not isinstance(exact, FlatIndex):
+        raise TypeError("refine_search: `exact` must be a paper_2401_08281_b200.FlatIndex")
+    if exact.d != fast.d:
+        raise ValueError(f"dimension mismatch: fast d={fast.d}, exact d={exact.d}")
+    metric = fast.metric
+    coarse = fast.search(q, shortlist)
+    dev = f"cuda:{exact.device}"
+    on_cuda = is_torch(q) and q.is_cuda
+    qt = q if is_torch(q) else torch.from_numpy(np.ascontiguousarray(q))
+    qt = qt.to(device=dev, dtype=torch.float32).contiguous()
+    cand = coarse.ids if is_torch(coarse.ids) else torch.from_numpy(np.ascontiguousarray(coarse.ids))
+    cand = cand.to(device=dev, dtype=torch.int64).contiguous()
+    nq = qt.shape[0]
+    D = torch.empty((nq, k), dtype=torch.float32, device=dev)
+    I = torch.empty((nq, k), dtype=torch.int64, device=dev)
+    N.check(N.lib().fk_refine(exact._h, metric.code, _ptr(qt), nq, _ptr(cand), int(cand.shape[1]), int(k),
+                              _ptr(D), _ptr(I), 1, _stream_of(exact.device)))
+    if on_cuda:
+        return SearchResult(I, D, k)
+    return SearchResult(I.cpu().numpy(), D.cpu().numpy(), k)
 
 
 class IndexFlatL2(FlatIndex):

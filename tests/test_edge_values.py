@@ -24,7 +24,25 @@ from parity import assert_parity
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-from paper_2401_08281_b200 import METRIC_IP, METRIC_L2, FlatIndex  # noqa: E402
+from paper_2401_08281_b200 import METRIC_IP, METRIC_L2, FlatIndex, config  # noqa: E402
+
+
+@pytest.fixture(autouse=True, params=["blas", "direct"])
+def path(request):
+    """Run every case on both FlatIndex._search branches (flat.py:58-62):
+    "blas" forces the fused GEMM + top-k kernel (blas_threshold 0) and is
+    checked against flat_search_blas; "direct" keeps the reference threshold
+    (these batches are < 20 queries) and is checked against the direct path."""
+    saved = config.blas_threshold
+    config.blas_threshold = 0 if request.param == "blas" else 20
+    yield request.param
+    config.blas_threshold = saved
+
+
+def oracle_search(xb, q, k, metric):
+    if config.blas_threshold == 0 or q.shape[0] >= config.blas_threshold:
+        return O.flat_search_blas(xb, q, k, metric)
+    return O.flat_search_direct(xb, q, k, metric)
 
 
 def assert_same_order(got_ids, got_dist, want_ids, want_dist):
@@ -74,7 +92,7 @@ def test_nan_inf_order_small(storage, metric):
     res = idx.search(q, nb)  # every row: the whole order is visible
     xr, qr = O.round_to(xb, storage), O.round_to(q, storage)
     with np.errstate(invalid="ignore", over="ignore"):
-        want_ids, want_dist = O.flat_search_blas(xr, qr, nb, metric)
+        want_ids, want_dist = oracle_search(xr, qr, nb, metric)
     assert_same_order(res.ids, res.distances, want_ids, want_dist)
     # NaN query: all NaN, ids by position
     assert np.all(np.isnan(res.distances[4]))
@@ -92,14 +110,14 @@ def test_nan_rows_small_k(metric):
     idx.add(xb)
     res = idx.search(q, 10)
     with np.errstate(invalid="ignore", over="ignore"):
-        want_ids, want_dist = O.flat_search_blas(xb, q, 10, metric)
+        want_ids, want_dist = oracle_search(xb, q, 10, metric)
     assert_same_order(res.ids, res.distances, want_ids, want_dist)
     if metric == "ip":
         assert np.array_equal(res.ids[0, :4], [3, 11, 12, nb - 1])
 
 
 @pytest.mark.parametrize("metric", ["l2", "ip"])
-def test_nan_inf_large_fp32_one_pass_path(metric):
+def test_nan_inf_large_fp32_one_pass_path(metric, path):
     """>= 262144 rows: the 1-pass TF32 + certified rescoring path with NaN /
     inf in the data (unbounded bands -> exact fallback) stays exact."""
     rng = np.random.default_rng(33)
@@ -108,9 +126,9 @@ def test_nan_inf_large_fp32_one_pass_path(metric):
     idx = FlatIndex(d, METRIC_L2 if metric == "l2" else METRIC_IP)
     idx.add(xb)
     res = idx.search(q, 10)
-    assert idx.last_plan()["kmode"] == 4
+    assert idx.last_plan()["kmode"] == (4 if path == "blas" else -1)
     with np.errstate(invalid="ignore", over="ignore"):
-        want_ids, want_dist = O.flat_search_blas(xb, q, 10, metric)
+        want_ids, want_dist = oracle_search(xb, q, 10, metric)
     assert_same_order(res.ids, res.distances, want_ids, want_dist)
 
 
@@ -140,6 +158,6 @@ def test_ip_signed_zero_order():
     idx = FlatIndex(d, METRIC_IP)
     idx.add(xb)
     res = idx.search(q, 5)
-    want_ids, want_dist = O.flat_search_blas(xb, q, 5, "ip")
+    want_ids, want_dist = oracle_search(xb, q, 5, "ip")
     assert np.array_equal(res.ids, want_ids)
     assert np.array_equal(res.distances, want_dist)
