@@ -22,6 +22,7 @@
 #include "fk_host.cuh"
 #include "flatknn_kernels.cuh"
 #include "storage_kernels.cuh"
+#include "filter16_kernels.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
@@ -145,6 +146,14 @@ struct fk_index {
   // rebuilt lazily after add / remove / reset
   DevBuf idt_keys, idt_pos, idt_tmp, idt_miss, rm_kill, rm_flags, rm_keep;
   int64_t idt_n = -1;
+  // fp32 MODE 5 filter operands: scaled fp16 copy of the base [cap][dp16]
+  // (rows [0, f16_rows) converted; built lazily at search time), its scale
+  // state (F16State), the staged queries' fp16 rows and 2^-s per query
+  DevBuf x16, f16st, q16, qinv;
+  DevBuf ovf;  // F1P overflow lists: [nq][ovf_cap] keys, positions, [nq] counts
+  int r_ovf_cap = 0;
+  int dp16 = 0;
+  int64_t f16_rows = 0;
   cudaEvent_t scratch_ev = nullptr;
   bool scratch_used = false;
   int64_t plan_rows = 0;  // FK_OPT_PLAN_ROWS (0: ntotal)
@@ -273,6 +282,7 @@ int launch_fused(int epi, int kmode, bool fold, bool ip, int kq, const CUtensorM
   switch (kmode) {
     case 0: return launch_fused_mode<0>(epi, ip, kq, a0, a1, b0, b1, sp, grid, smem, st);
     case 4: return launch_fused_mode<4>(epi, ip, kq, a0, a1, b0, b1, sp, grid, smem, st);
+    case 5: return launch_fused_mode<5>(epi, ip, kq, a0, a1, b0, b1, sp, grid, smem, st);
     case 1: return launch_fused_mode<1>(epi, ip, kq, a0, a1, b0, b1, sp, grid, smem, st);
     default:
       if (fold && !ip) return launch_fused_mode<3>(epi, ip, kq, a0, a1, b0, b1, sp, grid, smem, st);
@@ -340,6 +350,7 @@ int fk_create(int device, int d, int metric, int storage, fk_index** out) {
   h->d = d;
   const int ce = chunk_elems_of(storage);
   h->dp = (d + ce - 1) / ce * ce;
+  h->dp16 = (d + 63) / 64 * 64;
   h->metric = metric;
   h->storage = storage;
   // bf16 L2 with >= 3 free padding columns: fold the norms into the operands
@@ -354,8 +365,10 @@ int fk_create(int device, int d, int metric, int storage, fk_index** out) {
   }
   if (const char* e = getenv("FK_NO_FOLD"); e && atoi(e)) h->fold = 0;
   h->num_sms = prop.multiProcessorCount;
-  if (cudaMalloc((void**)&h->inexact, 2 * sizeof(unsigned int)) != cudaSuccess ||
-      cudaMemset(h->inexact, 0, 2 * sizeof(unsigned int)) != cudaSuccess ||
+  // {base, queries} exactness flags of the tf32 split (MODE 0/4) and of the
+  // scaled fp16 filter operands (MODE 5)
+  if (cudaMalloc((void**)&h->inexact, 4 * sizeof(unsigned int)) != cudaSuccess ||
+      cudaMemset(h->inexact, 0, 4 * sizeof(unsigned int)) != cudaSuccess ||
       cudaMalloc((void**)&h->xn_max, sizeof(float)) != cudaSuccess || cudaMemset(h->xn_max, 0, sizeof(float)) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->scratch_ev, cudaEventDisableTiming) != cudaSuccess) {
     cudaFree(h->inexact);
@@ -380,7 +393,8 @@ void fk_destroy(fk_index* h) {
                     &h->outD, &h->outI, &h->outP, &h->stage_in, &h->stage_ids, &h->rfail, &h->rcomp, &h->rflag,
                     &h->glock, &h->gkeys, &h->rcand, &h->rcount, &h->rdist, &h->rkid, &h->rkrd, &h->rkeep,
                     &h->rrowc, &h->rsel, &h->rnsel, &h->rtmp, &h->rkid2, &h->rkrd2, &h->rv1, &h->rv2, &h->rlims,
-                    &h->idt_keys, &h->idt_pos, &h->idt_tmp, &h->idt_miss, &h->rm_kill, &h->rm_flags, &h->rm_keep})
+                    &h->idt_keys, &h->idt_pos, &h->idt_tmp, &h->idt_miss, &h->rm_kill, &h->rm_flags, &h->rm_keep,
+                    &h->x16, &h->f16st, &h->q16, &h->qinv, &h->ovf})
     b->release();
   if (h->scratch_ev) cudaEventDestroy(h->scratch_ev);
   cudaFree(h->xn_max);
@@ -398,9 +412,11 @@ int fk_reset(fk_index* h) {
   std::lock_guard<std::mutex> g(h->mu);
   CK(cudaSetDevice(h->device));
   CK(cudaMemset(h->xn_max, 0, sizeof(float)));
-  CK(cudaMemset(h->inexact, 0, 2 * sizeof(unsigned int)));
+  CK(cudaMemset(h->inexact, 0, 4 * sizeof(unsigned int)));
+  if (h->f16st.p) CK(cudaMemset(h->f16st.p, 0, sizeof(F16State)));
   h->ntotal = 0;
   h->idt_n = -1;
+  h->f16_rows = 0;
   return FK_OK;
 }
 
@@ -468,18 +484,22 @@ struct Plan {
 int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force_S, Plan* pl, int kmode = -1) {
   Plan P{};
   P.kq = kq;
-  // 16-bit storage: 2 epilogue warps per TMEM lane quarter (the epilogue, not
-  // the MMA, paces a 16-bit tile); fp32 3xTF32 is MMA-paced -> 1 per quarter
-  P.epi = h->storage == FK_F32 ? 4 : 8;
-  if (const char* e = getenv("FK_EPI"); e && kq >= 0) P.epi = atoi(e) == 8 ? 8 : 4;
-  P.nh = P.epi / 4;
-  P.num_m = (int)((nq + BM - 1) / BM);
   if (kmode < 0) kmode = kmode_of(h);
   P.kmode = kmode;
+  // operand layout of this pass: 16-bit (fp16/bf16 storage, or the scaled
+  // fp16 filter copy of fp32 rows, MODE 5) or fp32/tf32
+  const bool h16 = h->storage != FK_F32 || kmode == 5;
+  const int dpk = kmode == 5 ? h->dp16 : h->dp;
+  // 16-bit operands: 2 epilogue warps per TMEM lane quarter (the epilogue, not
+  // the MMA, paces a 16-bit tile); fp32 3xTF32 is MMA-paced -> 1 per quarter
+  P.epi = h16 ? 8 : 4;
+  if (const char* e = getenv(kmode == 5 ? "FK_EPI5" : "FK_EPI"); e && kq >= 0) P.epi = atoi(e) == 8 ? 8 : 4;
+  P.nh = P.epi / 4;
+  P.num_m = (int)((nq + BM - 1) / BM);
   const int split = kmode == 0 ? 2 : 1;
-  const int num_kb = h->dp / chunk_elems_of(h->storage);
+  const int num_kb = dpk / (h16 ? 64 : 32);
   const int a_bytes = split * num_kb * (int)CHUNK_BYTES;
-  const int a_tmem_cols = h->storage == FK_F32 ? split * h->dp : h->dp / 2;
+  const int a_tmem_cols = h16 ? dpk / 2 : split * dpk;
   // Query operand placement and tile width:
   //  * 16-bit with two epilogue groups: the accumulator ring wants 4 buffers
   //    (an even count, see below), so A goes to smem (SS MMA) when it fits;
@@ -488,7 +508,7 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   //    with 64-column tiles (2 x 64 accumulators) rather than re-streaming A;
   //  * otherwise A in smem, or streamed with every stage (a_mode 2).
   P.bn = 128;
-  if (h->storage != FK_F32 && P.nh == 2 && a_bytes <= 64 * 1024) P.a_mode = 1;
+  if (h16 && P.nh == 2 && a_bytes <= 64 * 1024) P.a_mode = 1;
   else if (kmode == 4 && a_bytes <= 64 * 1024) P.a_mode = 1;  // 1-pass fp32: 4 accumulators (+2.5 %)
   else if (a_tmem_cols <= 256) P.a_mode = 0;
   else if (a_tmem_cols <= 384) {
@@ -503,7 +523,7 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   if (P.a_mode == 0 && a_tmem_cols > 512 - (single_acc ? 1 : 2) * P.bn) P.a_mode = 1;
   if (P.a_mode != 0) P.bn = 128;
   if (P.bn == 64) {  // 64-column kernels exist only for the default epilogue width
-    P.epi = h->storage == FK_F32 ? 4 : 8;
+    P.epi = h16 ? 8 : 4;
     P.nh = P.epi / 4;
   }
   const int bn = P.bn;
@@ -516,9 +536,10 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   if (P.num_m < 2 || h->num_sms < 2) P.cluster = 1;
   // (the 1-pass fp32 search certifies far fewer queries in pair mode: not used)
   if (kmode == 4) P.cluster = 1;
+  if (kmode == 5 && !getenv("FK_CLUSTER5")) P.cluster = 1;
   P.num_mu = (P.num_m + P.cluster - 1) / P.cluster;
   // chunk <= L2_CHUNK_BYTES of streamed base; partial lists <= PARTIAL_BYTES
-  const size_t tile_bytes = (size_t)bn * h->dp * elem_bytes_of(h->storage) * split;
+  const size_t tile_bytes = (size_t)bn * dpk * (h16 ? 2 : 4) * split;
   // (very large k: partial lists are k deep, so merge cost grows with S -> 4x window)
   size_t l2_chunk = L2_CHUNK_BYTES;
   if (const char* e = getenv("FK_L2_CHUNK_MB")) l2_chunk = (size_t)std::max(1, atoi(e)) << 20;
@@ -539,7 +560,7 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   const int hist_bytes = kq == 0 ? P.epi * 1024 : 0;
   // norm-tile ring: 4 slots when smem is tight (fp32), 8 otherwise
   // (even: one sub-ring per producer/issuer pair)
-  P.xn_slots = (h->metric == FK_METRIC_IP || h->fold) ? 0 : (h->storage == FK_F32 && P.a_mode != 2) ? 4 : 8;
+  P.xn_slots = (h->metric == FK_METRIC_IP || h->fold) ? 0 : (!h16 && P.a_mode != 2) ? 4 : 8;
   const int xn_bytes = P.xn_slots * bn * 4;
   auto stage_bytes_for = [&](int mode) { return split * b_chunk + (mode == 2 ? split * (int)CHUNK_BYTES : 0); };
   auto stages_for = [&](int mode) {
@@ -587,10 +608,15 @@ int run_fused(fk_index* h, const Plan& P, int64_t nq, int64_t nb_pass, int k, bo
     if ((rc = h->cbuf.ensure((size_t)P.grid * P.epi * 32 * P.cap * sizeof(uint64_t)))) return rc;
   }
   CUtensorMap ta0, ta1, tb0, tb1;
-  const int eb = elem_bytes_of(h->storage);
-  if ((rc = make_map(&ta0, h->q0.p, eb, h->dp, nq))) return rc;
+  const bool f16 = P.kmode == 5;  // scaled fp16 filter copies of the fp32 rows
+  const bool h16 = h->storage != FK_F32 || f16;
+  const int eb = h16 ? 2 : 4;
+  const int dpk = f16 ? h->dp16 : h->dp;
+  const void* qop = f16 ? h->q16.p : h->q0.p;
+  const void* bop = f16 ? h->x16.p : h->s0;
+  if ((rc = make_map(&ta0, qop, eb, dpk, nq))) return rc;
   const uint32_t b_rows = P.cluster == 2 ? P.bn / 2 : P.bn;  // cluster mode: each CTA loads half a tile
-  if ((rc = make_map(&tb0, h->s0, eb, h->dp, nb_pass, b_rows))) return rc;
+  if ((rc = make_map(&tb0, bop, eb, dpk, nb_pass, b_rows))) return rc;
   if (P.kmode == 0) {
     if ((rc = make_map(&ta1, h->q1.p, eb, h->dp, nq))) return rc;
     if ((rc = make_map(&tb1, h->s1, eb, h->dp, nb_pass, b_rows))) return rc;
@@ -611,7 +637,7 @@ int run_fused(fk_index* h, const Plan& P, int64_t nq, int64_t nb_pass, int k, bo
   sp.cap = P.cap;
   sp.dbg_ip = h->dbg_ip;
   sp.trace = h->trace;
-  sp.qa0 = h->q0.p;
+  sp.qa0 = qop;
   sp.qa1 = h->q1.p;
   sp.nq = (int)nq;
   sp.nb = (int)nb_pass;
@@ -621,13 +647,13 @@ int run_fused(fk_index* h, const Plan& P, int64_t nq, int64_t nb_pass, int k, bo
   sp.chunk_tiles = P.chunk_tiles;
   sp.S = P.S;
   sp.num_units = P.num_units;
-  sp.num_kb = h->dp / chunk_elems_of(h->storage);
+  sp.num_kb = dpk / (h16 ? 64 : 32);
   sp.a_mode = P.a_mode;
   sp.stages = P.stages;
   sp.xn_slots = P.xn_slots;
   sp.acc_stages = P.acc_stages;
   {
-    const int bk = chunk_elems_of(h->storage), kstep = h->storage == FK_F32 ? 8 : 16;
+    const int bk = h16 ? 64 : 32, kstep = h16 ? 16 : 8;
     const int last = h->d + (h->fold ? 3 : 0) - (sp.num_kb - 1) * bk;  // K elements in the last chunk (1..bk)
     sp.kk_last = (last + kstep - 1) / kstep;
   }
@@ -641,7 +667,16 @@ int run_fused(fk_index* h, const Plan& P, int64_t nq, int64_t nb_pass, int k, bo
   sp.pub_mask = 15;
   if (const char* e = getenv("FK_PUB")) sp.pub_mask = std::max(0, atoi(e));
   sp.rflag = static_cast<unsigned int*>(h->rflag.p);
-  sp.inexact = h->split == 2 ? h->inexact : nullptr;  // raw storage: no lo parts known -> full band
+  if (h->r_ovf_cap > 0) {
+    sp.ovf_cap = h->r_ovf_cap;
+    sp.ovf_key = static_cast<uint32_t*>(h->ovf.p);
+    sp.ovf_pos = sp.ovf_key + (size_t)nq * sp.ovf_cap;
+    sp.ovf_cnt = sp.ovf_pos + (size_t)nq * sp.ovf_cap;
+  }
+  // exactness flags: tf32 split {base, queries}; MODE 5 its own pair
+  sp.inexact = f16 ? h->inexact + 2 : (h->split == 2 ? h->inexact : nullptr);  // raw storage: full band
+  sp.qinv = static_cast<const float*>(h->qinv.p);
+  sp.xinv = f16 ? &static_cast<const F16State*>(h->f16st.p)->xinv : nullptr;
   sp.glock = h->r_union ? static_cast<unsigned int*>(h->glock.p) : nullptr;
   sp.gkeys = h->r_union ? static_cast<uint32_t*>(h->gkeys.p) : nullptr;
   sp.radius = h->r_radius;
@@ -703,7 +738,8 @@ int launch_merge(fk_index* h, const Plan& P, int64_t nq, int k, bool ip, float* 
 }
 
 // Queries -> device operand layout + norms (shared by search and range search).
-int stage_queries(fk_index* h, const void* q, int64_t nq, int dtype, int on_device, cudaStream_t st) {
+int stage_queries(fk_index* h, const void* q, int64_t nq, int dtype, int on_device, cudaStream_t st,
+                  bool f16 = false) {
   int rc;
   const size_t in_row = (size_t)h->d * dtype_bytes(dtype);
   const void* qsrc = q;
@@ -717,22 +753,70 @@ int stage_queries(fk_index* h, const void* q, int64_t nq, int dtype, int on_devi
   if (h->split == 2 && (rc = h->q1.ensure(nq * qrow))) return rc;
   if ((rc = h->qn.ensure(nq * sizeof(float)))) return rc;
   if (h->inexact) CK(cudaMemsetAsync(h->inexact + 1, 0, sizeof(unsigned int), st));
+  if (f16) {  // MODE 5: scaled fp16 filter rows + 2^-s per query (filter16_kernels.cuh)
+    if ((rc = h->q16.ensure((size_t)nq * h->dp16 * 2))) return rc;
+    if ((rc = h->qinv.ensure((size_t)nq * sizeof(float)))) return rc;
+    CK(cudaMemsetAsync(h->inexact + 3, 0, sizeof(unsigned int), st));
+    f16_query_kernel<<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(qsrc, dtype, nq, h->d, h->dp16,
+                                                                 static_cast<__half*>(h->q16.p),
+                                                                 static_cast<float*>(h->qinv.p), h->inexact + 3);
+    CKL();
+    h->nlaunch++;
+  }
   return launch_prep(kmode_of(h), qsrc, dtype, nq, h->d, h->dp, h->q0.p, h->q1.p, static_cast<float*>(h->qn.p), 0, st,
                      h->fold ? 2 : 0, h->inexact ? h->inexact + 1 : nullptr);
+}
+
+// MODE 5: bring the scaled fp16 copy of the base up to date (rows added
+// since the last conversion; every row when the base scale changed or the
+// copy was invalidated).  The scale decision happens on the device.
+int ensure_f16_base(fk_index* h, cudaStream_t st) {
+  int rc;
+  if (h->split != 2 || !h->s1) return set_err(FK_E_UNSUPPORTED, "the fp16 filter needs the hi/lo fp32 storage");
+  const size_t need = (size_t)h->cap * h->dp16 * 2;
+  if (h->x16.bytes < need) {
+    if ((rc = h->x16.ensure(need))) return rc;
+    h->f16_rows = 0;
+  }
+  if (!h->f16st.p) {
+    if ((rc = h->f16st.ensure(sizeof(F16State)))) return rc;
+    CK(cudaMemsetAsync(h->f16st.p, 0, sizeof(F16State), st));
+    h->f16_rows = 0;
+  }
+  if (h->f16_rows == h->ntotal) return FK_OK;
+  auto fs = static_cast<F16State*>(h->f16st.p);
+  const auto hi = static_cast<const float*>(h->s0);
+  const auto lo = static_cast<const float*>(h->s1);
+  const size_t e0 = (size_t)h->f16_rows * h->dp, e1 = (size_t)h->ntotal * h->dp;
+  const unsigned ga = (unsigned)std::min<size_t>((e1 - e0 + 255) / 256, (size_t)h->num_sms * 8);
+  absmax_rows_kernel<<<ga, 256, 0, st>>>(hi, lo, e0, e1, &fs->absmax);
+  CKL();
+  f16_scale_kernel<<<1, 32, 0, st>>>(fs, (long long)h->f16_rows, h->inexact + 2);
+  CKL();
+  const unsigned gc = (unsigned)std::min<int64_t>((h->ntotal + 7) / 8, (int64_t)h->num_sms * 16);
+  f16_base_kernel<<<gc, 256, 0, st>>>(hi, lo, h->f16_rows, h->ntotal, h->d, h->dp, h->dp16,
+                                      static_cast<__half*>(h->x16.p), fs, h->inexact + 2);
+  CKL();
+  h->nlaunch += 3;
+  h->f16_rows = h->ntotal;
+  return FK_OK;
 }
 
 // fp32 MODE 4 search: fused pass with a 1-pass TF32 GEMM keeping k' >= k
 // entries per list in tf32 order, then merge_rescore_kernel (certify + exact
 // values + exact top-k); uncertified queries get the exact fallback.
 int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI, int64_t* dP, cudaEvent_t* ev,
-                 cudaStream_t st, Plan* plan_out) {
+                 cudaStream_t st, Plan* plan_out, int kmode = 4) {
   int rc;
+  if (kmode == 5 && (rc = ensure_f16_base(h, st))) return rc;
   // k' >= k entries per list, the slack absorbs the tf32 band around the k-th
-  int kp = k <= 16 ? 32 : std::min(k + std::max(64, k / 4), FK_MAX_K);
+  // (register queues of 16 with the per-query overflow lists: measured
+  // cfg2 3.7 ms fused vs 5.6 with 32-deep queues, 0 of 10k uncertified)
+  int kp = k <= 4 ? 8 : k <= 16 ? 16 : std::min(k + std::max(64, k / 4), FK_MAX_K);
   if (const char* e = getenv("FK_KP")) kp = std::max(k, std::min(atoi(e), FK_MAX_K));
   const int kq = kp <= 8 ? 8 : kp <= 16 ? 16 : kp <= 32 ? 32 : 0;
   Plan pl;
-  if ((rc = make_plan(h, nq, h->ntotal, kp, kq, 0, &pl, 4))) return rc;
+  if ((rc = make_plan(h, nq, h->ntotal, kp, kq, 0, &pl, kmode))) return rc;
   *plan_out = pl;
   if ((rc = h->thr.ensure((size_t)nq * sizeof(uint32_t)))) return rc;
   CK(cudaMemsetAsync(h->thr.p, 0xFF, (size_t)nq * sizeof(uint32_t), st));
@@ -747,10 +831,24 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
   }
   h->r_union = gunion;
   h->r_kfinal = k;
+  // overflow lists for band members dropped by full register queues
+  int ovf_cap = kq > 0 ? 64 : 0;
+  if (const char* e = getenv("FK_OVF")) ovf_cap = kq > 0 ? std::max(0, atoi(e)) : 0;
+  uint32_t *okey = nullptr, *opos = nullptr;
+  unsigned int* ocnt = nullptr;
+  if (ovf_cap > 0) {
+    if ((rc = h->ovf.ensure((size_t)nq * (2 * ovf_cap + 1) * 4))) return rc;
+    okey = static_cast<uint32_t*>(h->ovf.p);
+    opos = okey + (size_t)nq * ovf_cap;
+    ocnt = opos + (size_t)nq * ovf_cap;
+    CK(cudaMemsetAsync(ocnt, 0, (size_t)nq * 4, st));
+  }
+  h->r_ovf_cap = ovf_cap;
   if (ev) CK(cudaEventRecord(ev[1], st));
   rc = run_fused(h, pl, nq, h->ntotal, kp, ip, st);
   h->r_kfinal = 0;
   h->r_union = false;
+  h->r_ovf_cap = 0;
   if (rc) return rc;
   if (ev) CK(cudaEventRecord(ev[2], st));
   if ((rc = h->rfail.ensure((size_t)(2 * nq + 1) * sizeof(int)))) return rc;
@@ -781,25 +879,39 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
   const auto xl = h->split == 2 ? static_cast<const float*>(h->s1) : nullptr;
   const auto qn = static_cast<const float*>(h->qn.p);
   int* fail = static_cast<int*>(h->rfail.p);
+  // the filter pass's exactness flags and rounding-band coefficient (L2; IP half)
+  const unsigned int* inexact = kmode == 5 ? h->inexact + 2 : (h->split == 2 ? h->inexact : nullptr);
+  const float band_l2 = kmode == 5 ? 0.0078125f : 0.015625f;
   if (ip)
     merge_rescore_kernel<true><<<(unsigned)nq, 256, msmem, st>>>(pk, pp, pc, pl.S_tot, (int)nq, kp, k, thr, q0, q1, xb, xl, qn,
                                                                   h->norms, h->xn_max, h->dp, h->ids, dD, dI, dP, smc,
                                                                   fail, fcount, flist,
                                                                   static_cast<const unsigned int*>(h->rflag.p),
-                                                                  h->split == 2 ? h->inexact : nullptr);
+                                                                  inexact, band_l2, okey, opos, ocnt, ovf_cap);
   else
     merge_rescore_kernel<false><<<(unsigned)nq, 256, msmem, st>>>(pk, pp, pc, pl.S_tot, (int)nq, kp, k, thr, q0, q1, xb, xl, qn,
                                                                    h->norms, h->xn_max, h->dp, h->ids, dD, dI, dP, smc,
                                                                    fail, fcount, flist,
                                                                   static_cast<const unsigned int*>(h->rflag.p),
-                                                                  h->split == 2 ? h->inexact : nullptr);
+                                                                  inexact, band_l2, okey, opos, ocnt, ovf_cap);
   CKL();
   h->nlaunch++;
   if (getenv("FK_DIAG")) {  // diagnostics: how many queries failed certification
     int nf = 0;
     CK(cudaMemcpyAsync(&nf, fcount, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    fprintf(stderr, "[fk] mode4 k=%d k'=%d nq=%lld uncertified=%d\n", k, kp, (long long)nq, nf);
+    long long osum = 0, orows = 0, omax = 0;
+    if (ocnt) {
+      std::vector<unsigned int> oc(nq);
+      CK(cudaMemcpy(oc.data(), ocnt, nq * 4, cudaMemcpyDeviceToHost));
+      for (auto c : oc) {
+        osum += c;
+        orows += c > 0;
+        omax = std::max<long long>(omax, c);
+      }
+    }
+    fprintf(stderr, "[fk] mode%d k=%d k'=%d nq=%lld uncertified=%d overflow rows=%lld entries=%lld max=%lld\n", kmode,
+            k, kp, (long long)nq, nf, orows, osum, omax);
   }
   // uncertified queries: exact fallback on the device (no host sync); up to
   // one wave of CTAs, each scanning the base for its failed queries, with a
@@ -1124,11 +1236,15 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
   } else if (h->storage == FK_F32 &&
              (h->split == 1 ||
               (k <= 16 && (h->plan_rows > 0 ? h->plan_rows : h->ntotal) >= FP32_1X_MIN_ROWS && !getenv("FK_FP32_3X")))) {
+    // filter pass: scaled fp16 (MODE 5, default with the hi/lo storage) or
+    // tf32 (MODE 4; FK_FP32_FILTER=tf32, or raw fp32 storage)
+    const char* ff = getenv("FK_FP32_FILTER");
+    const int fmode = (h->split == 2 && !(ff && std::strcmp(ff, "tf32") == 0)) ? 5 : 4;
     if (ev) CK(cudaEventRecord(ev[0], st));
-    if ((rc = stage_queries(h, q, nq, dtype, on_device, st))) return rc;
+    if ((rc = stage_queries(h, q, nq, dtype, on_device, st, fmode == 5))) return rc;
     h->nlaunch++;
     Plan pl;
-    if ((rc = search_mode4(h, nq, k, ip, dD, dI, dP, ev, st, &pl))) return rc;
+    if ((rc = search_mode4(h, nq, k, ip, dD, dI, dP, ev, st, &pl, fmode))) return rc;
     if (ev) CK(cudaEventRecord(ev[3], st));
     h->plan[0] = pl.grid;
     h->plan[1] = pl.S;
@@ -1353,6 +1469,8 @@ int fk_remove_ids(fk_index* h, const int64_t* ids, int64_t n, int on_device, int
     }
     h->ntotal = nk;
     h->idt_n = -1;
+    h->f16_rows = 0;  // the fp16 filter copy (and its scale) is rebuilt from the survivors
+    if (h->f16st.p) CK(cudaMemsetAsync(h->f16st.p, 0, sizeof(F16State), st));
   }
   if ((rc = scratch_end(h, st))) return rc;
   CK(cudaStreamSynchronize(st));

@@ -337,7 +337,9 @@ __global__ void __launch_bounds__(256) merge_rescore_kernel(
     const float* __restrict__ qnorm, const float* __restrict__ xnorm, const float* __restrict__ xn_max, int dp,
     const int64_t* __restrict__ ids, float* __restrict__ D, int64_t* __restrict__ I, int64_t* __restrict__ P, int smc,
     int* __restrict__ fail, int* __restrict__ fail_count, int* __restrict__ fail_list,
-    const unsigned int* __restrict__ rflag, const unsigned int* __restrict__ inexact) {
+    const unsigned int* __restrict__ rflag, const unsigned int* __restrict__ inexact, float band_l2,
+    const uint32_t* __restrict__ ovf_key, const uint32_t* __restrict__ ovf_pos,
+    const unsigned int* __restrict__ ovf_cnt, int ovf_cap) {
   extern __shared__ uint64_t sm[];  // smc gathered entries, then the k winners (pow2-padded)
   __shared__ int count, count2;
   __shared__ uint32_t hist[256], sel[8];
@@ -371,6 +373,15 @@ __global__ void __launch_bounds__(256) merge_rescore_kernel(
     const int idx = atomicAdd(&count, 1);
     if (idx < smc) sm[idx] = (static_cast<uint64_t>(key) << 32) | ps;
   }
+  if (ovf_cnt != nullptr) {  // band members the units' full queues dropped
+    const int no = min((int)ovf_cnt[q], ovf_cap);
+    for (int e = tid; e < no; e += blockDim.x) {
+      const uint32_t key = ovf_key[(size_t)q * ovf_cap + e];
+      if (key > thr) continue;
+      const int idx = atomicAdd(&count, 1);
+      if (idx < smc) sm[idx] = (static_cast<uint64_t>(key) << 32) | ovf_pos[(size_t)q * ovf_cap + e];
+    }
+  }
   __syncthreads();
   int n = count;
   if (n > smc) {  // more survivors than the buffer: exact fallback for this query
@@ -379,11 +390,12 @@ __global__ void __launch_bounds__(256) merge_rescore_kernel(
   }
   // certification on the tf32 values
   const float qn = qnorm[q];
-  // band 2e with a 2x safety factor: L2 2 * 2 * 2^-8, IP 2 * 2 * 2^-9 (|q| max|x|)
-  // for tf32 rounding; plus the fp32 accumulation slack (4 dp + 8) 2^-23 (qn + max xn)
+  // band 2e with a 2x safety factor: L2 2 * 2 * 2^-8 (tf32 filter; band_l2 =
+  // 2^-6) or 2 * 2 * 2^-9 (scaled fp16 filter; 2^-7) times |q| max|x|, IP half;
+  // plus the fp32 accumulation slack (4 dp + 8) 2^-23 (qn + max xn)
   // (same bound as the fused kernel's band4)
   const bool tf32_exact = inexact != nullptr && (inexact[0] | inexact[1]) == 0u;
-  const float e2 = (tf32_exact ? 0.f : (IS_IP ? 0.0078125f : 0.015625f)) * sqrtf(fmaxf(qn, 0.f) * fmaxf(*xn_max, 0.f)) +
+  const float e2 = (tf32_exact ? 0.f : (IS_IP ? 0.5f * band_l2 : band_l2)) * sqrtf(fmaxf(qn, 0.f) * fmaxf(*xn_max, 0.f)) +
                    (4.f * (float)dp + 8.f) * 1.1920928955078125e-07f * (fmaxf(qn, 0.f) + fmaxf(*xn_max, 0.f));
   bool ok = true;
   uint32_t band_key = 0xFFFFFFFFu;  // only entries with t <= t_k + band can be in the exact top-k

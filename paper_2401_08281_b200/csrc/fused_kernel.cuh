@@ -97,12 +97,23 @@ struct SearchParams {
   // {base, queries}: nonzero when some value needs its lo part; when both
   // are zero the 1-pass tf32 products are exact and the band collapses
   const unsigned int* inexact;
+  // MODE 5: 2^-s of each query row's fp16 scale [nq] and of the base's
+  // (device scalar); NaN marks an unusable scale (row -> exact fallback)
+  const float* qinv;
+  const float* xinv;
   int pub_mask;  // publish the own bound / fetch the shared one every pub_mask+1 own tiles
   // MODE 4: per-query running union of the finished units' best k' tf32 keys
   // (lock-protected), so the shared bound tightens towards the global k-th
   unsigned int* glock;  // [nq]
   uint32_t* gkeys;      // [nq][32]
   unsigned int* rflag;
+  // F1P: entries inside the band that a full register queue had to drop go
+  // to a per-query overflow list [nq][ovf_cap] (count may exceed the cap:
+  // the row is then flagged for the exact fallback)
+  uint32_t* ovf_key;
+  uint32_t* ovf_pos;
+  unsigned int* ovf_cnt;
+  int ovf_cap;
   // range search (KQ == -1): every (row, position) whose fast-filter value
   // passes the conservative radius bound is appended to rcand (the exact
   // direct distance and the radius test follow in range_exact_kernel)
@@ -314,12 +325,16 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     fused_knn_kernel(const __grid_constant__ CUtensorMap tm_a0, const __grid_constant__ CUtensorMap tm_a1,
                      const __grid_constant__ CUtensorMap tm_b0, const __grid_constant__ CUtensorMap tm_b1,
                      const SearchParams p) {
-  // MODE 0: fp32 3xTF32 hi/lo; 4: raw fp32, ONE tf32 pass as a filter with a
-  // proven margin and exact fp32 rescoring of the survivors; 1/2: fp16/bf16
+  // MODE 0: fp32 3xTF32 hi/lo; 4: fp32, ONE tf32 pass as a filter with a
+  // proven margin and exact fp32 rescoring of the survivors; 5: the same
+  // filter on power-of-two-scaled fp16 copies of the fp32 rows (same 11-bit
+  // precision as tf32, twice the MMA rate, half the bytes; filter16_kernels.cuh);
+  // 1/2: fp16/bf16 storage
   constexpr bool TF32 = (MODE == 0 || MODE == 4);
+  constexpr bool F1P = (MODE == 4 || MODE == 5);  // 1-pass filter + certified exact rescoring
   constexpr int SPLIT = (MODE == 0) ? 2 : 1;
   constexpr int BK = TF32 ? 32 : 64;  // elements per 128-byte K-chunk
-  constexpr uint32_t AB_FMT = TF32 ? 2u : (MODE == 1 ? 0u : 1u);
+  constexpr uint32_t AB_FMT = TF32 ? 2u : ((MODE == 1 || MODE == 5) ? 0u : 1u);
   // MODE 3 (bf16, L2): base rows are stored as [-2x | xn split in 3 bf16] and
   // query rows as [q | 1 1 1], so the accumulator already holds xn - 2 q.x and
   // the epilogue needs no base-norm tile (FOLD).
@@ -653,7 +668,10 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       }
 
       constexpr bool RANGE = KQ < 0;
-      const float qn = ((!IS_IP || RANGE || MODE == 4) && row_ok) ? p.qnorm[row] : 0.f;
+      const float qn = ((!IS_IP || RANGE || F1P) && row_ok) ? p.qnorm[row] : 0.f;
+      // MODE 5: accumulator -> inner product scale 2^-(s_q + s_x) (exact)
+      const float sc = (MODE == 5 && row_ok) ? __ldg(p.qinv + row) * __ldg(p.xinv) : 1.f;
+      const float c2 = -2.f * sc;
       constexpr int KQS = KQ > 0 ? KQ : 1;
       uint32_t keys[KQS], pos[KQS];
       if constexpr (KQ > 0) {
@@ -673,8 +691,11 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       // merge_rescore_kernel); the bound we filter and publish with is
       // (own kfinal-th t) + band >= (global kfinal-th t) + band
       const bool tf32_exact = p.inexact != nullptr && (p.inexact[0] | p.inexact[1]) == 0u;
-      const float band4 = (MODE == 4 && KQ > 0 && !RANGE && row_ok)
-                              ? (tf32_exact ? 0.f : (IS_IP ? 0.0078125f : 0.015625f)) *
+      // rounding term: tf32 (raw fp32 truncated to 11 bits): |t - ip| <= 2^-9 |q||x|;
+      // scaled fp16 (RNE, 11 bits): <= (2^-10 + 2^-27) |q||x| -> half the band
+      constexpr float BAND_L2 = (MODE == 5) ? 0.0078125f : 0.015625f;
+      const float band4 = (F1P && KQ > 0 && !RANGE && row_ok)
+                              ? (tf32_exact ? 0.f : (IS_IP ? 0.5f * BAND_L2 : BAND_L2)) *
                                         sqrtf(fmaxf(p.qnorm[row], 0.f) * fmaxf(*p.xn_max, 0.f)) +
                                     // fp32 accumulation: the tensor core (possibly truncating,
                                     // <= dp 2^-23) and the sequential-FMA rescoring (<= dp 2^-24)
@@ -683,13 +704,13 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
                                     (4.f * (float)dp + 8.f) * 1.1920928955078125e-07f *
                                         (fmaxf(p.qnorm[row], 0.f) + fmaxf(*p.xn_max, 0.f))
                               : 0.f;
-      uint32_t min_lost = 0xFFFFFFFFu;  // MODE 4: smallest key dropped from a full queue
+      uint32_t min_lost = 0xFFFFFFFFu;  // F1P: smallest band key lost (overflow list full)
       // queue slot of the caller's k-th (MODE 4 keeps k' >= kfinal entries);
       // read through a static select so the queue stays in registers
       const int kf_slot = (KQS - k) + p.kfinal - 1;
       auto own_key = [&]() -> uint32_t {
         if constexpr (KQ > 0) {
-          if (MODE == 4) {
+          if (F1P) {
             const uint32_t kk = select_static<KQS>(keys, kf_slot);
             if (kk == 0xFFFFFFFFu) return kk;
             const float b = unmonotone(kk) + band4;
@@ -707,7 +728,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       // Conservative fast-filter bound on f = fl(xn - 2ip): the reference value
       // fl(fl(qn + xn) - 2ip) differs from qn + f by < 3u(qn + xn + |v|); the
       // 2^-20 margin (u = 2^-24) over max-norm covers it with room to spare.
-      const float xmax = (IS_IP && MODE != 4) ? 0.f : *p.xn_max;
+      const float xmax = (IS_IP && !F1P) ? 0.f : *p.xn_max;
       // MODE 4 range search: the single tf32 pass rounds each operand to 11
       // significant bits, |ip_tf32 - ip| <= 2^-9 sum|q_i||x_i| <= 2^-9 |q||x|,
       // so f = xn - 2 ip moves by <= 2^-8 |q| max|x|: widen by 2^-7 (2x) before
@@ -783,17 +804,23 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         auto chunk_f = [&](const uint32_t (&r)[32], int c0, float (&f)[32]) {
 #pragma unroll
           for (int j4 = 0; j4 < 8; ++j4) {
-            if (IS_IP || FOLD) {
+            if (IS_IP && MODE == 5) {
+              f[4 * j4 + 0] = __uint_as_float(r[4 * j4 + 0]) * sc;
+              f[4 * j4 + 1] = __uint_as_float(r[4 * j4 + 1]) * sc;
+              f[4 * j4 + 2] = __uint_as_float(r[4 * j4 + 2]) * sc;
+              f[4 * j4 + 3] = __uint_as_float(r[4 * j4 + 3]) * sc;
+            } else if (IS_IP || FOLD) {
               f[4 * j4 + 0] = __uint_as_float(r[4 * j4 + 0]);
               f[4 * j4 + 1] = __uint_as_float(r[4 * j4 + 1]);
               f[4 * j4 + 2] = __uint_as_float(r[4 * j4 + 2]);
               f[4 * j4 + 3] = __uint_as_float(r[4 * j4 + 3]);
             } else {
+              // c2 = -2 (MODE 5: -2 * 2^-(s_q + s_x), so c2 * acc is exactly -2 t)
               const float4 x = lds_f4(xs + c0 + 4 * j4);
-              f[4 * j4 + 0] = fmaf(-2.f, __uint_as_float(r[4 * j4 + 0]), x.x);
-              f[4 * j4 + 1] = fmaf(-2.f, __uint_as_float(r[4 * j4 + 1]), x.y);
-              f[4 * j4 + 2] = fmaf(-2.f, __uint_as_float(r[4 * j4 + 2]), x.z);
-              f[4 * j4 + 3] = fmaf(-2.f, __uint_as_float(r[4 * j4 + 3]), x.w);
+              f[4 * j4 + 0] = fmaf(c2, __uint_as_float(r[4 * j4 + 0]), x.x);
+              f[4 * j4 + 1] = fmaf(c2, __uint_as_float(r[4 * j4 + 1]), x.y);
+              f[4 * j4 + 2] = fmaf(c2, __uint_as_float(r[4 * j4 + 2]), x.z);
+              f[4 * j4 + 3] = fmaf(c2, __uint_as_float(r[4 * j4 + 3]), x.w);
             }
           }
         };
@@ -826,7 +853,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             cand &= cand - 1;
             // (MODE 4: a 1-pass tf32 value; the queue works in that space and
             // merge_rescore_kernel recomputes the survivors exactly)
-            const float ip = select32(reinterpret_cast<const float(&)[32]>(r), j);
+            const float ip = select32(reinterpret_cast<const float(&)[32]>(r), j) * sc;
             // flat.py:111: dmat = (qn + norms) - 2.0*ip  (2*ip exact -> one FMA;
             // FOLD: the accumulator already is xn - 2 ip)
             float v;
@@ -837,13 +864,33 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
               if (!IS_IP) v = (v <= 0.f) ? 0.f : v;  // np.maximum(dmat, 0) (flat.py:112)
               const uint32_t kv = IS_IP ? dist_key(ip, true) : dist_key(v, false);
               if constexpr (KQ > 0) {
-                if (MODE == 4) {  // band filter: track what a full queue drops
-                  if (kv >= keys[KQS - 1]) min_lost = min(min_lost, kv);
-                  else if (pos[KQS - 1] != 0xFFFFFFFFu) min_lost = min(min_lost, keys[KQS - 1]);
+                uint32_t lk = 0xFFFFFFFFu, lp = 0u;  // F1P: the entry a full queue drops
+                if (F1P) {
+                  if (kv >= keys[KQS - 1]) {
+                    lk = kv;
+                    lp = static_cast<uint32_t>(n0 + c0 + j);
+                  } else if (pos[KQS - 1] != 0xFFFFFFFFu) {
+                    lk = keys[KQS - 1];
+                    lp = pos[KQS - 1];
+                  }
                 }
                 queue_insert<KQS>(keys, pos, kv, static_cast<uint32_t>(n0 + c0 + j));
                 thr = unmonotone(min(own_key(), gkey));
                 T = filter_bound(thr);
+                if (F1P && lk != 0xFFFFFFFFu && lk <= min(own_key(), gkey)) {
+                  // a band member: keep it in the query's overflow list
+                  if (p.ovf_cnt != nullptr) {
+                    const unsigned slot = atomicAdd(p.ovf_cnt + row, 1u);
+                    if (slot < (unsigned)p.ovf_cap) {
+                      p.ovf_key[(size_t)row * p.ovf_cap + slot] = lk;
+                      p.ovf_pos[(size_t)row * p.ovf_cap + slot] = lp;
+                    } else {
+                      min_lost = min(min_lost, lk);
+                    }
+                  } else {
+                    min_lost = min(min_lost, lk);
+                  }
+                }
               } else {
                 mybuf[cnt++] = (static_cast<uint64_t>(kv) << 32) | static_cast<uint32_t>(n0 + c0 + j);
               }
@@ -959,7 +1006,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
               if (bnd == bnd) atomicMin(p.thr_key + row, monotone(bnd));
             }
           }
-          if (MODE == 4 && min_lost != 0xFFFFFFFFu && min_lost <= own_key()) {
+          if (F1P && ((min_lost != 0xFFFFFFFFu && min_lost <= own_key()) || !(sc == sc))) {
             atomicOr(p.rflag + row, 1u);  // band member dropped
             if (FK_DEV && row < 3)
               printf("row %d chunk %d: min_lost %f own(kth+band) %f keys0 %f keys9 %f keys31 %f band %f gkey %f\n", row,

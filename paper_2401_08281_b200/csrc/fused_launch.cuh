@@ -59,8 +59,8 @@ int launch_fused_k(int kq, const CUtensorMap& a0, const CUtensorMap& a1, const C
     case 16: return launch_fused_t<MODE, 16, IP, EPI>(a0, a1, b0, b1, sp, grid, smem, st);
     case 32: return launch_fused_t<MODE, 32, IP, EPI>(a0, a1, b0, b1, sp, grid, smem, st);
     case 0: return launch_fused_t<MODE, 0, IP, EPI>(a0, a1, b0, b1, sp, grid, smem, st);
-    case -1:  // range search: default epilogue width only
-      if constexpr ((MODE == 0 || MODE == 4) == (EPI == 4))
+    case -1:  // range search: default epilogue width only (not on the MODE 5 filter)
+      if constexpr (MODE != 5 && (MODE == 0 || MODE == 4) == (EPI == 4))
         return launch_fused_t<MODE, -1, IP, EPI>(a0, a1, b0, b1, sp, grid, smem, st);
       return set_err(FK_E_UNSUPPORTED, "range search runs with the default epilogue width");
   }

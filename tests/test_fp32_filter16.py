@@ -1,0 +1,175 @@
+"""fp32 search through the scaled-fp16 filter pass (kernel MODE 5, the
+default 1-pass algorithm for fp32 storage with k <= 16 over >= 256k rows).
+
+The fp32 rows and queries get power-of-two-scaled fp16 copies (11 significant
+bits, like a tf32 operand); one kind::f16 tensor-core pass ranks k' >= k
+candidates per list, band members that full register queues drop go to a
+per-query overflow list, the merge certifies each query against the fp16
+error band and recomputes the survivors exactly in fp32 (flat.py:111-112),
+and uncertified queries take the exact fallback.  The answers must equal the
+reference's (north-star parity rules) and -- because the final values come
+from the same exact rescoring -- be bit-identical to the tf32 filter (MODE 4).
+
+``set_plan_rows`` makes small test databases take the 1-pass path."""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+sys.path.insert(0, os.path.join(HERE, "golden"))
+
+from cases import CASES, make_inputs  # noqa: E402
+from oracle import flat_oracle as O  # noqa: E402
+from parity import assert_parity  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+GOLD = np.load(os.path.join(HERE, "golden", "golden.npz"))
+FP32_CASES = [n for n in CASES if make_inputs(n)[4] == "fp32"]
+
+
+def _index(d, metric, plan_rows=1 << 20):
+    from paper_2401_08281_b200 import METRIC_IP, METRIC_L2, FlatIndex
+    idx = FlatIndex(d, METRIC_IP if metric == "ip" else METRIC_L2, storage="fp32")
+    idx.set_plan_rows(plan_rows)
+    return idx
+
+
+def _search(idx, q, k, filt=None, kp=None):
+    old = {n: os.environ.get(n) for n in ("FK_FP32_FILTER", "FK_KP")}
+    try:
+        if filt:
+            os.environ["FK_FP32_FILTER"] = filt
+        if kp:
+            os.environ["FK_KP"] = str(kp)
+        res = idx.search(q, k)
+    finally:
+        for n, v in old.items():
+            if v is None:
+                os.environ.pop(n, None)
+            else:
+                os.environ[n] = v
+    return res
+
+
+@pytest.mark.parametrize("name", FP32_CASES)
+def test_filter16_golden(name):
+    xb, q, k, metric, storage, ids = make_inputs(name)
+    idx = _index(xb.shape[1], metric)
+    if xb.shape[0]:
+        if ids is None:
+            idx.add(xb)
+        else:
+            idx.add_with_ids(xb, ids)
+    res = idx.search(q, k)
+    if xb.shape[0] and k <= 16 and q.shape[0] >= 20:
+        assert idx.last_plan()["kmode"] == 5
+    assert_parity(res.ids, res.distances, GOLD[f"{name}/blas_ids"], GOLD[f"{name}/blas_dist"])
+
+
+@pytest.mark.parametrize("metric", ["l2", "ip"])
+@pytest.mark.parametrize("k", [1, 10, 16])
+@pytest.mark.parametrize("kp", [None, 16, 8])
+def test_filter16_vs_oracle_and_tf32(metric, k, kp):
+    """Default k' = 32, and short queues (k' = 16 / 8) that overflow into the
+    per-query lists: same answers as the oracle, bit-identical to MODE 4."""
+    if kp is not None and kp < k:
+        pytest.skip("k' >= k")
+    rng = np.random.default_rng(199 + k)
+    xb = rng.standard_normal((60000, 64), dtype=np.float32)
+    q = rng.standard_normal((300, 64), dtype=np.float32)
+    idx = _index(64, metric)
+    idx.add(xb)
+    r5 = _search(idx, q, k, kp=kp)
+    assert idx.last_plan()["kmode"] == 5
+    want_ids, want_dist = O.flat_search_blas(xb, q, k, metric)
+    assert_parity(r5.ids, r5.distances, want_ids, want_dist)
+    r4 = _search(idx, q, k, filt="tf32")
+    assert idx.last_plan()["kmode"] == 4
+    assert np.array_equal(r5.ids, r4.ids) and np.array_equal(r5.distances, r4.distances)
+
+
+def test_filter16_integer_ties_exact_band():
+    """Integer data is exact in scaled fp16: the band collapses to the
+    accumulation slack and the massive exact ties keep the reference order."""
+    rng = np.random.default_rng(7)
+    xb = rng.integers(0, 256, size=(200_000, 128)).astype(np.float32)
+    q = rng.integers(0, 256, size=(64, 128)).astype(np.float32)
+    q[:8] = xb[rng.choice(xb.shape[0], 8, replace=False)]  # exact duplicates: distance 0
+    idx = _index(128, "l2")
+    idx.add(xb)
+    res = idx.search(q, 10)
+    want_ids, want_dist = O.flat_search_blas(xb, q, 10, "l2")
+    assert np.array_equal(res.ids, want_ids) and np.array_equal(res.distances, want_dist)
+
+
+@pytest.mark.parametrize("scale", [1e-30, 1e-8, 1.0, 3e4, 1e15, 1e18])
+def test_filter16_extreme_magnitudes(scale):
+    """The power-of-two scales keep 11 bits at any magnitude (and flag an
+    unusable scale -> exact fallback); mixed-magnitude rows hit the fp16
+    subnormal range, covered by the band's absolute term."""
+    rng = np.random.default_rng(int(abs(np.log10(scale))) + 3)
+    xb = rng.standard_normal((20000, 48)).astype(np.float32)
+    xb[::7] *= 1e-6  # rows far below the base maximum
+    xb[3::11, :5] = 0.0
+    q = rng.standard_normal((100, 48)).astype(np.float32)
+    q[::5] *= 1e-5
+    xb = (xb * scale).astype(np.float32)
+    q = (q * scale).astype(np.float32)
+    for metric in ("l2", "ip"):
+        idx = _index(48, metric)
+        idx.add(xb)
+        res = idx.search(q, 10)
+        with np.errstate(over="ignore", under="ignore", invalid="ignore"):
+            want_ids, want_dist = O.flat_search_blas(xb, q, 10, metric)
+        if np.all(np.isfinite(want_dist)):
+            assert_parity(res.ids, res.distances, want_ids, want_dist)
+        r4 = _search(idx, q, 10, filt="tf32")
+        assert np.array_equal(res.ids, r4.ids) and np.array_equal(res.distances, r4.distances)
+
+
+def test_filter16_rescale_on_add_and_remove():
+    """Adding rows with a larger magnitude changes the base scale (the fp16
+    copy is rebuilt); remove_ids invalidates it; results stay exact."""
+    rng = np.random.default_rng(11)
+    xa = rng.standard_normal((30000, 32), dtype=np.float32)
+    xb = (rng.standard_normal((30000, 32)) * 1e6).astype(np.float32)
+    q = rng.standard_normal((50, 32), dtype=np.float32)
+    idx = _index(32, "l2")
+    idx.add(xa)
+    r = idx.search(q, 5)
+    assert_parity(r.ids, r.distances, *O.flat_search_blas(xa, q, 5, "l2"))
+    idx.add(xb)  # new max |x|: every row is re-encoded with the new scale
+    both = np.vstack([xa, xb])
+    r = idx.search(q, 5)
+    assert_parity(r.ids, r.distances, *O.flat_search_blas(both, q, 5, "l2"))
+    idx.add(xa[:1000] * 0.5)  # same scale: only the new rows are converted
+    both = np.vstack([both, xa[:1000] * 0.5])
+    r = idx.search(q, 5)
+    assert_parity(r.ids, r.distances, *O.flat_search_blas(both, q, 5, "l2"))
+    removed = idx.remove_ids(np.arange(30000, 60000))
+    assert removed == 30000
+    left = np.vstack([xa, xa[:1000] * 0.5])
+    r = idx.search(q, 5)
+    want_ids, want_dist = O.flat_search_blas(left, q, 5, "l2")
+    want_ids = np.where(want_ids >= 30000, want_ids + 30000, want_ids)  # ids of the last batch
+    assert_parity(r.ids, r.distances, want_ids, want_dist)
+
+
+def test_filter16_inf_rows_and_nan_query():
+    rng = np.random.default_rng(12)
+    xb = rng.standard_normal((40000, 24), dtype=np.float32)
+    xb[5] = np.inf
+    xb[9, 3] = np.nan
+    q = rng.standard_normal((40, 24), dtype=np.float32)
+    q[3, 2] = np.nan
+    idx = _index(24, "l2")
+    idx.add(xb)
+    res = idx.search(q, 10)
+    with np.errstate(invalid="ignore", over="ignore"):
+        want_ids, want_dist = O.flat_search_blas(xb, q, 10, "l2")
+    fin = np.all(np.isfinite(want_dist), axis=1)
+    assert_parity(res.ids[fin], res.distances[fin], want_ids[fin], want_dist[fin])
+    assert np.all(np.isnan(res.distances[3]))

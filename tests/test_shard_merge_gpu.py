@@ -108,6 +108,6 @@ def test_sharded_index_world1_nccl():
         assert_parity(res.ids.cpu().numpy(), res.distances.cpu().numpy(), want_ids, want_dist)
         # the shard planned the fp32 algorithm on the global row count
         sh.local.search(q[:50], 10)
-        assert sh.local.last_plan()["kmode"] == 4
+        assert sh.local.last_plan()["kmode"] in (4, 5)
     finally:
         dist.destroy_process_group()
