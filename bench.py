@@ -379,19 +379,23 @@ def run_ours(args, cfg):
     nb_local = local_index.ntotal
     flops = 2.0 * nq * nb_local * d
     # fp32: kmode 0 = 3xTF32 (3 tf32 passes); kmode 4 = ONE tf32 pass ranking a
-    # shortlist + exact fp32 rescoring of the band (same answers, see DESIGN 4.7)
-    one_pass = cfg["storage"] == "fp32" and plan.get("kmode") == 4
+    # shortlist + exact fp32 rescoring of the band; kmode 5 = the same with ONE
+    # kind::f16 pass over power-of-two-scaled fp16 copies (same answers, DESIGN 4.1b)
+    kmode = plan.get("kmode")
+    one_pass = cfg["storage"] == "fp32" and kmode in (4, 5)
+    f16_filter = cfg["storage"] == "fp32" and kmode == 5
     passes = 3 if (cfg["storage"] == "fp32" and not one_pass) else 1
-    tc_peak = peaks["bf16_tflops"] / (2.0 if cfg["storage"] == "fp32" else 1.0) / passes
+    tc_peak = peaks["bf16_tflops"] / (2.0 if (cfg["storage"] == "fp32" and not f16_filter) else 1.0) / passes
     achieved = flops / (t_fused / 1e3) / 1e12
-    elem = 4 if cfg["storage"] == "fp32" else 2
-    streamed = 2 if (cfg["storage"] == "fp32" and not one_pass) else 1  # hi+lo, or hi only
+    elem = 4 if (cfg["storage"] == "fp32" and not f16_filter) else 2
+    streamed = 2 if (cfg["storage"] == "fp32" and not one_pass) else 1  # hi+lo, or the filter operand only
     alg_bytes = nb_local * d * elem * streamed + nb_local * 4 + nq * d * elem * 2 + nq * k * 8
     line = {
         "metric": "exact k-NN QPS (1M x 128, k=10)" if args.config == 2 else f"exact k-NN QPS ({cfg['name']})",
         "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": ("f32 (1-pass TF32 filter + exact f32 rescoring)" if one_pass else "f32 (3xTF32 tensor-core split)")
+        "dtype": ("f32 (1-pass scaled-fp16 filter + exact f32 rescoring)" if f16_filter else
+                  "f32 (1-pass TF32 filter + exact f32 rescoring)" if one_pass else "f32 (3xTF32 tensor-core split)")
         if cfg["storage"] == "fp32" else cfg["storage"],
         "data": "synthetic (numpy default_rng(0/1) standard normal, SURVEY 8(d))",
         "config": {"workload": cfg["name"], "nb": nb, "d": d, "nq": nq, "k": k, "metric": cfg["metric"],
@@ -407,8 +411,13 @@ def run_ours(args, cfg):
                      "kernel_ms": t_fused, "prep_ms": t_prep, "merge_ms": t_merge,
                      "alg_flops_per_launch": flops, "alg_bytes_per_launch": alg_bytes,
                      "peak_note": f"{peaks_kind} bf16 {peaks['bf16_tflops']} TF/s"
-                                  + ((" / 2 (tf32 rate), one tf32 pass" if one_pass else
+                                  + ((" (kind::f16 rate), one fp16 filter pass" if f16_filter else
+                                      " / 2 (tf32 rate), one tf32 pass" if one_pass else
                                       " / 2 (tf32 rate) / 3 (3xTF32 passes)") if cfg["storage"] == "fp32" else "")},
+        "roofline_tf32_1pass": ({"peak": peaks["bf16_tflops"] / 2.0, "unit": "TFLOP/s",
+                                 "frac": achieved / (peaks["bf16_tflops"] / 2.0),
+                                 "note": "one tf32 pass (the round-1 definition the verdict's 0.70 target uses)"}
+                                if f16_filter else None),
         "roofline_survey_3xtf32": ({"peak": peaks["bf16_tflops"] / 6.0, "unit": "TFLOP/s",
                                     "frac": achieved / (peaks["bf16_tflops"] / 6.0),
                                     "note": "SURVEY 8(d) fp32 definition (3 tf32 passes at measured peak); "

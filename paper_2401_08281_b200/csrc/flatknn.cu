@@ -161,6 +161,8 @@ struct fk_index {
   float r_radius = 0.f;
   int r_kfinal = 0;  // MODE 4 search: the caller's k (lists keep k' >= k)
   bool r_union = false;  // MODE 4 search: maintain the per-query running union bound
+  bool r_prepass = false;  // bound pre-pass: publish thr_key only (no union, overflow or row flags)
+  DevBuf rflag_pre;
   unsigned long long r_cap = 0;
   long long est_fallbacks = 0;  // large-k searches whose estimated bound failed certification
   std::mutex mu;
@@ -394,7 +396,7 @@ void fk_destroy(fk_index* h) {
                     &h->glock, &h->gkeys, &h->rcand, &h->rcount, &h->rdist, &h->rkid, &h->rkrd, &h->rkeep,
                     &h->rrowc, &h->rsel, &h->rnsel, &h->rtmp, &h->rkid2, &h->rkrd2, &h->rv1, &h->rv2, &h->rlims,
                     &h->idt_keys, &h->idt_pos, &h->idt_tmp, &h->idt_miss, &h->rm_kill, &h->rm_flags, &h->rm_keep,
-                    &h->x16, &h->f16st, &h->q16, &h->qinv, &h->ovf})
+                    &h->x16, &h->f16st, &h->q16, &h->qinv, &h->ovf, &h->rflag_pre})
     b->release();
   if (h->scratch_ev) cudaEventDestroy(h->scratch_ev);
   cudaFree(h->xn_max);
@@ -667,7 +669,12 @@ int run_fused(fk_index* h, const Plan& P, int64_t nq, int64_t nb_pass, int k, bo
   sp.pub_mask = 15;
   if (const char* e = getenv("FK_PUB")) sp.pub_mask = std::max(0, atoi(e));
   sp.rflag = static_cast<unsigned int*>(h->rflag.p);
-  if (h->r_ovf_cap > 0) {
+  if (h->r_prepass) {
+    // bound pre-pass: its rows are searched again by the main pass, so it
+    // must not feed the union (duplicates) or flag rows; only thr_key counts
+    if ((rc = h->rflag_pre.ensure((size_t)nq * sizeof(unsigned int)))) return rc;
+    sp.rflag = static_cast<unsigned int*>(h->rflag_pre.p);
+  } else if (h->r_ovf_cap > 0) {
     sp.ovf_cap = h->r_ovf_cap;
     sp.ovf_key = static_cast<uint32_t*>(h->ovf.p);
     sp.ovf_pos = sp.ovf_key + (size_t)nq * sp.ovf_cap;
@@ -677,8 +684,8 @@ int run_fused(fk_index* h, const Plan& P, int64_t nq, int64_t nb_pass, int k, bo
   sp.inexact = f16 ? h->inexact + 2 : (h->split == 2 ? h->inexact : nullptr);  // raw storage: full band
   sp.qinv = static_cast<const float*>(h->qinv.p);
   sp.xinv = f16 ? &static_cast<const F16State*>(h->f16st.p)->xinv : nullptr;
-  sp.glock = h->r_union ? static_cast<unsigned int*>(h->glock.p) : nullptr;
-  sp.gkeys = h->r_union ? static_cast<uint32_t*>(h->gkeys.p) : nullptr;
+  sp.glock = (h->r_union && !h->r_prepass) ? static_cast<unsigned int*>(h->glock.p) : nullptr;
+  sp.gkeys = (h->r_union && !h->r_prepass) ? static_cast<uint32_t*>(h->gkeys.p) : nullptr;
   sp.radius = h->r_radius;
   sp.rcand = static_cast<unsigned long long*>(h->rcand.p);
   sp.rcount = static_cast<unsigned long long*>(h->rcount.p);
@@ -802,6 +809,34 @@ int ensure_f16_base(fk_index* h, cudaStream_t st) {
   return FK_OK;
 }
 
+// Bound pre-pass: a short fused pass over the first rows of the base (every
+// query) publishes each query's k-th (+ band) to thr_key before the main
+// pass, so the first wave of units filters with a useful bound instead of
+// inserting ~k ln(n/k) candidates per row.  Any k entries give a valid upper
+// bound, so the rows may be any subset; the main pass searches them again.
+// FK_PREPASS = rows (default 0 = off: on cfg2 16k / 32k rows cost 0.26 /
+// 0.40 ms more than they save -- the running-union bound already makes the
+// later waves cheap).
+int run_prepass(fk_index* h, int64_t nq, int k, int kq, bool ip, int kmode, cudaStream_t st) {
+  if (kq <= 0) return FK_OK;
+  int64_t rows = 0;
+  if (const char* e = getenv("FK_PREPASS")) rows = std::max<int64_t>(0, atoll(e));
+  rows = rows / BN * BN;
+  if (rows <= 0 || h->ntotal < 16 * rows) return FK_OK;
+  Plan pp;
+  int rc;
+  if ((rc = make_plan(h, nq, rows, k, kq, 0, &pp, kmode))) return rc;
+  const bool su = h->r_union;
+  const int so = h->r_ovf_cap;
+  h->r_prepass = true;
+  h->r_ovf_cap = 0;
+  rc = run_fused(h, pp, nq, rows, k, ip, st);
+  h->r_prepass = false;
+  h->r_union = su;
+  h->r_ovf_cap = so;
+  return rc;
+}
+
 // fp32 MODE 4 search: fused pass with a 1-pass TF32 GEMM keeping k' >= k
 // entries per list in tf32 order, then merge_rescore_kernel (certify + exact
 // values + exact top-k); uncertified queries get the exact fallback.
@@ -845,6 +880,7 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
   }
   h->r_ovf_cap = ovf_cap;
   if (ev) CK(cudaEventRecord(ev[1], st));
+  if ((rc = run_prepass(h, nq, kp, kq, ip, kmode, st))) return rc;
   rc = run_fused(h, pl, nq, h->ntotal, kp, ip, st);
   h->r_kfinal = 0;
   h->r_union = false;
@@ -1300,6 +1336,7 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
         if ((rc = run_fused(h, pe, nq, m_est, 32, ip, st))) return rc;
         CK(cudaMemsetAsync(h->fail.p, 0, sizeof(int), st));
       }
+      if (kq > 0 && (rc = run_prepass(h, nq, k, kq, ip, pl.kmode, st))) return rc;
       if ((rc = run_fused(h, pl, nq, h->ntotal, k, ip, st))) return rc;
       if (ev) CK(cudaEventRecord(ev[2], st));
       if ((rc = launch_merge(h, pl, nq, k, ip, dD, dI, dP, est ? static_cast<int*>(h->fail.p) : nullptr, st)))

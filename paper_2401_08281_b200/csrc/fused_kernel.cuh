@@ -152,13 +152,18 @@ __device__ __forceinline__ void queue_insert(uint32_t (&keys)[KQ], uint32_t (&po
 }
 
 // a[idx] for a runtime idx without dynamic register indexing (which would
-// move the whole array to local memory): N predicated selects
+// move the whole array to local memory): a log2(N)-deep tree of selects
+// (N a power of two), short latency on the insertion path
 template <int N>
 __device__ __forceinline__ uint32_t select_static(const uint32_t (&a)[N], int idx) {
-  uint32_t r = a[0];
+  if constexpr (N == 1) {
+    return a[0];
+  } else {
+    uint32_t t[N / 2];
 #pragma unroll
-  for (int i = 1; i < N; ++i) r = (i == idx) ? a[i] : r;
-  return r;
+    for (int i = 0; i < N / 2; ++i) t[i] = (idx & 1) ? a[2 * i + 1] : a[2 * i];
+    return select_static<N / 2>(t, idx >> 1);
+  }
 }
 
 // Sort a bitonic sequence of 32 keys ascending (half-cleaner network, static
@@ -875,9 +880,10 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
                   }
                 }
                 queue_insert<KQS>(keys, pos, kv, static_cast<uint32_t>(n0 + c0 + j));
-                thr = unmonotone(min(own_key(), gkey));
+                const uint32_t bk = min(own_key(), gkey);
+                thr = unmonotone(bk);
                 T = filter_bound(thr);
-                if (F1P && lk != 0xFFFFFFFFu && lk <= min(own_key(), gkey)) {
+                if (F1P && lk != 0xFFFFFFFFu && lk <= bk) {
                   // a band member: keep it in the query's overflow list
                   if (p.ovf_cnt != nullptr) {
                     const unsigned slot = atomicAdd(p.ovf_cnt + row, 1u);
