@@ -94,6 +94,11 @@ constexpr size_t PARTIAL_BYTES = 4ull << 30;    // split-N partial top-k lists
 constexpr int MERGE_SMC = 16384;    // large-k merge: survivors gathered in smem (128 KB) + 2048 winners
 constexpr int SMEM_RESERVE = 1024 /*align*/ + 512 /*barriers + tmem slot*/;
 
+// largest k served by the 1-pass filter + rescoring path (FK_FP32_1PASS_MAXK)
+int fp32_1pass_max_k() {
+  if (const char* e = getenv("FK_FP32_1PASS_MAXK")) return atoi(e);
+  return 16;
+}
 int elem_bytes_of(int storage) { return storage == FK_F32 ? 4 : 2; }
 int chunk_elems_of(int storage) { return storage == FK_F32 ? 32 : 64; }
 int split_of(int storage) { return storage == FK_F32 ? 2 : 1; }
@@ -1271,7 +1276,8 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
     h->plan[11] = -1;  // direct path
   } else if (h->storage == FK_F32 &&
              (h->split == 1 ||
-              (k <= 16 && (h->plan_rows > 0 ? h->plan_rows : h->ntotal) >= FP32_1X_MIN_ROWS && !getenv("FK_FP32_3X")))) {
+              (k <= fp32_1pass_max_k() && (h->plan_rows > 0 ? h->plan_rows : h->ntotal) >= FP32_1X_MIN_ROWS &&
+               !getenv("FK_FP32_3X")))) {
     // filter pass: scaled fp16 (MODE 5, default with the hi/lo storage) or
     // tf32 (MODE 4; FK_FP32_FILTER=tf32, or raw fp32 storage)
     const char* ff = getenv("FK_FP32_FILTER");

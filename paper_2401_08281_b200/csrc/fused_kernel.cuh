@@ -121,7 +121,8 @@ struct SearchParams {
   unsigned long long* rcand;  // [rcap] (row << 32 | position)
   unsigned long long* rcount; // device counter (may exceed rcap: caller grows and reruns)
   unsigned long long rcap;
-  int dbg_flags;   // bottleneck experiments: 1 = epilogue skips compute, 2 = producer skips TMA
+  int dbg_flags;   // bottleneck experiments (FK_DEBUG_FLAGS): 1 = epilogue skips TMEM loads + compute,
+                   // 2 = producer skips TMA, 4 = no slow path, 8 = TMEM loads without the filter
 };
 
 // ------------------------------------------------------------ register queue
@@ -481,7 +482,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
               rph ^= 1;
             }
             mbar_wait(&empty[stage], phase ^ 1);
-            if (FK_DEV && (p.dbg_flags & 2)) {  // experiment: no data movement
+            if (p.dbg_flags & 2) {  // experiment: no data movement
               mbar_arrive(&full[stage]);
               continue;
             }
@@ -907,7 +908,8 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         // piece (2) hand the TMEM buffer back to the MMA issuer; (3) filter +
         // select from registers.  Tiles alternate between warp groups, so a
         // group has NG tile periods to finish one tile.
-        const bool do_epi = !(FK_DEV && (p.dbg_flags & 1));
+        const bool do_epi = !(p.dbg_flags & 1);
+        const bool do_cmp = do_epi && !(p.dbg_flags & 8);  // 8: TMEM loads without the filter
 #pragma unroll
         for (int pc = 0; pc < BN / PIECE; ++pc) {
           uint32_t racc[PIECE];
@@ -925,7 +927,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[buf]);
           }
-          if (do_epi) {
+          if (do_cmp) {
             if (p.dbg_ip != nullptr && row_ok) {
               for (int j = 0; j < PIECE; ++j)
                 if (pc * PIECE + j < nvalid) p.dbg_ip[(size_t)row * p.nb + n0 + pc * PIECE + j] = __uint_as_float(racc[j]);
@@ -943,7 +945,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
               mcs[c] = mc;
               m = (c == 0) ? mc : fmin_nan(m, mc);
             }
-            const bool slow = !(m > T) && row_ok && !(FK_DEV && (p.dbg_flags & 4));
+            const bool slow = !(m > T) && row_ok && !(p.dbg_flags & 4);
             if (FK_DEV && p.trace != nullptr) {
               const unsigned sb = __ballot_sync(FULLMASK, slow);
               if (tr) p.trace[tcount * 16 + 8] += __popc(sb);
