@@ -822,24 +822,34 @@ int ensure_f16_base(fk_index* h, cudaStream_t st) {
 // FK_PREPASS = rows (default 0 = off: on cfg2 16k / 32k rows cost 0.26 /
 // 0.40 ms more than they save -- the running-union bound already makes the
 // later waves cheap).
+// One bound-only fused pass over base rows [0, rows): lists of `k` entries
+// (queue bucket kq), publishing (kfinal-th + band) per query to thr_key; no
+// union, overflow lists or row flags (its rows are searched again).
+int run_bound_pass(fk_index* h, int64_t nq, int64_t rows, int k, int kq, int kfinal, bool ip, int kmode,
+                   cudaStream_t st) {
+  Plan pp;
+  int rc;
+  if ((rc = make_plan(h, nq, rows, k, kq, 0, &pp, kmode))) return rc;
+  const bool su = h->r_union;
+  const int so = h->r_ovf_cap, sk = h->r_kfinal;
+  h->r_prepass = true;
+  h->r_ovf_cap = 0;
+  h->r_kfinal = kfinal;
+  rc = run_fused(h, pp, nq, rows, k, ip, st);
+  h->r_prepass = false;
+  h->r_union = su;
+  h->r_ovf_cap = so;
+  h->r_kfinal = sk;
+  return rc;
+}
+
 int run_prepass(fk_index* h, int64_t nq, int k, int kq, bool ip, int kmode, cudaStream_t st) {
   if (kq <= 0) return FK_OK;
   int64_t rows = 0;
   if (const char* e = getenv("FK_PREPASS")) rows = std::max<int64_t>(0, atoll(e));
   rows = rows / BN * BN;
   if (rows <= 0 || h->ntotal < 16 * rows) return FK_OK;
-  Plan pp;
-  int rc;
-  if ((rc = make_plan(h, nq, rows, k, kq, 0, &pp, kmode))) return rc;
-  const bool su = h->r_union;
-  const int so = h->r_ovf_cap;
-  h->r_prepass = true;
-  h->r_ovf_cap = 0;
-  rc = run_fused(h, pp, nq, rows, k, ip, st);
-  h->r_prepass = false;
-  h->r_union = su;
-  h->r_ovf_cap = so;
-  return rc;
+  return run_bound_pass(h, nq, rows, k, kq, h->r_kfinal > 0 ? h->r_kfinal : k, ip, kmode, st);
 }
 
 // fp32 MODE 4 search: fused pass with a 1-pass TF32 GEMM keeping k' >= k
@@ -886,6 +896,16 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
   h->r_ovf_cap = ovf_cap;
   if (ev) CK(cudaEventRecord(ev[1], st));
   if ((rc = run_prepass(h, nq, kp, kq, ip, kmode, st))) return rc;
+  if (kq == 0 && !getenv("FK_NO_EST")) {
+    // large k: seed each query's bound with (32nd filter value of a sample of
+    // m = 8 ntotal / k rows) + band -- near the 4k-th overall for unordered
+    // data -- so the lists the merge gathers stay ~4k deep; the merge
+    // certifies bound > t_k + band per query (else the exact fallback)
+    int64_t m_est = ((h->ntotal * 8) / k + BN - 1) / BN * BN;
+    if (m_est >= 32 * BN && m_est * 8 <= h->ntotal &&
+        (rc = run_bound_pass(h, nq, m_est, 32, 32, 32, ip, kmode, st)))
+      return rc;
+  }
   rc = run_fused(h, pl, nq, h->ntotal, kp, ip, st);
   h->r_kfinal = 0;
   h->r_union = false;

@@ -173,3 +173,31 @@ def test_filter16_inf_rows_and_nan_query():
     fin = np.all(np.isfinite(want_dist), axis=1)
     assert_parity(res.ids[fin], res.distances[fin], want_ids[fin], want_dist[fin])
     assert np.all(np.isnan(res.distances[3]))
+
+
+@pytest.mark.parametrize("metric", ["l2", "ip"])
+@pytest.mark.parametrize("k,nb", [(32, 80_000), (100, 80_000), (1024, 600_000)])
+def test_filter16_large_k(metric, k, nb):
+    """k > 16 through the 1-pass filter (FK_FP32_1PASS_MAXK): large-k
+    candidate lists (KQ = 0), the sampled bound pass (600k rows, k = 1024)
+    and the certified rescoring merge -- same answers as the oracle and
+    bit-identical to the tf32 filter."""
+    rng = np.random.default_rng(500 + k)
+    xb = rng.standard_normal((nb, 32), dtype=np.float32)
+    q = rng.standard_normal((64, 32), dtype=np.float32)
+    idx = _index(32, metric)
+    idx.add(xb)
+    old = os.environ.get("FK_FP32_1PASS_MAXK")
+    os.environ["FK_FP32_1PASS_MAXK"] = "2048"
+    try:
+        r5 = idx.search(q, k)
+        assert idx.last_plan()["kmode"] == 5
+        r4 = _search(idx, q, k, filt="tf32")
+    finally:
+        if old is None:
+            os.environ.pop("FK_FP32_1PASS_MAXK")
+        else:
+            os.environ["FK_FP32_1PASS_MAXK"] = old
+    want_ids, want_dist = O.flat_search_blas(xb, q, k, metric)
+    assert_parity(r5.ids, r5.distances, want_ids, want_dist)
+    assert np.array_equal(r5.ids, r4.ids) and np.array_equal(r5.distances, r4.distances)
