@@ -94,6 +94,16 @@ constexpr size_t PARTIAL_BYTES = 4ull << 30;    // split-N partial top-k lists
 constexpr int MERGE_SMC = 16384;    // large-k merge: survivors gathered in smem (128 KB) + 2048 winners
 constexpr int SMEM_RESERVE = 1024 /*align*/ + 512 /*barriers + tmem slot*/;
 
+// Rounding-band coefficient of the 1-pass filter (times |q| max|x|, L2; IP
+// half): 2 x (filter-value error bound) with a 2^-10 margin -- scaled fp16
+// (MODE 5): 2 x 2 x (2^-10 + 2^-27) -> 2^-8; tf32 truncation (MODE 4):
+// 2 x 2 x (2^-9 + 2^-20) -> 2^-7.  FK_BAND scales it (experiments, >= 1).
+float f1p_band(int kmode) {
+  float b = (kmode == 5 ? 0.00390625f : 0.0078125f) * (1.f + 0.0009765625f);
+  if (const char* e = getenv("FK_BAND")) b *= std::max(1.f, (float)atof(e));
+  return b;
+}
+
 // largest k served by the 1-pass filter + rescoring path (FK_FP32_1PASS_MAXK)
 int fp32_1pass_max_k() {
   if (const char* e = getenv("FK_FP32_1PASS_MAXK")) return atoi(e);
@@ -166,7 +176,7 @@ struct fk_index {
   float r_radius = 0.f;
   int r_kfinal = 0;  // MODE 4 search: the caller's k (lists keep k' >= k)
   bool r_union = false;  // MODE 4 search: maintain the per-query running union bound
-  bool r_prepass = false;  // bound pre-pass: publish thr_key only (no union, overflow or row flags)
+  bool r_prepass = false;  // bound pass: publish thr_key only (no overflow lists or row flags; the union only when asked)
   DevBuf rflag_pre;
   unsigned long long r_cap = 0;
   long long est_fallbacks = 0;  // large-k searches whose estimated bound failed certification
@@ -688,9 +698,10 @@ int run_fused(fk_index* h, const Plan& P, int64_t nq, int64_t nb_pass, int k, bo
   // exactness flags: tf32 split {base, queries}; MODE 5 its own pair
   sp.inexact = f16 ? h->inexact + 2 : (h->split == 2 ? h->inexact : nullptr);  // raw storage: full band
   sp.qinv = static_cast<const float*>(h->qinv.p);
+  sp.band_l2 = f1p_band(P.kmode);
   sp.xinv = f16 ? &static_cast<const F16State*>(h->f16st.p)->xinv : nullptr;
-  sp.glock = (h->r_union && !h->r_prepass) ? static_cast<unsigned int*>(h->glock.p) : nullptr;
-  sp.gkeys = (h->r_union && !h->r_prepass) ? static_cast<uint32_t*>(h->gkeys.p) : nullptr;
+  sp.glock = h->r_union ? static_cast<unsigned int*>(h->glock.p) : nullptr;
+  sp.gkeys = h->r_union ? static_cast<uint32_t*>(h->gkeys.p) : nullptr;
   sp.radius = h->r_radius;
   sp.rcand = static_cast<unsigned long long*>(h->rcand.p);
   sp.rcount = static_cast<unsigned long long*>(h->rcount.p);
@@ -826,13 +837,14 @@ int ensure_f16_base(fk_index* h, cudaStream_t st) {
 // (queue bucket kq), publishing (kfinal-th + band) per query to thr_key; no
 // union, overflow lists or row flags (its rows are searched again).
 int run_bound_pass(fk_index* h, int64_t nq, int64_t rows, int k, int kq, int kfinal, bool ip, int kmode,
-                   cudaStream_t st) {
+                   cudaStream_t st, bool use_union = false) {
   Plan pp;
   int rc;
   if ((rc = make_plan(h, nq, rows, k, kq, 0, &pp, kmode))) return rc;
   const bool su = h->r_union;
   const int so = h->r_ovf_cap, sk = h->r_kfinal;
   h->r_prepass = true;
+  h->r_union = use_union;  // union of disjoint sample rows: valid when the main pass does not read it
   h->r_ovf_cap = 0;
   h->r_kfinal = kfinal;
   rc = run_fused(h, pp, nq, rows, k, ip, st);
@@ -902,9 +914,16 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
     // data -- so the lists the merge gathers stay ~4k deep; the merge
     // certifies bound > t_k + band per query (else the exact fallback)
     int64_t m_est = ((h->ntotal * 8) / k + BN - 1) / BN * BN;
-    if (m_est >= 32 * BN && m_est * 8 <= h->ntotal &&
-        (rc = run_bound_pass(h, nq, m_est, 32, 32, 32, ip, kmode, st)))
-      return rc;
+    // (the sample's units and epilogue groups each see part of it: their
+    // lists merge into the per-query union, whose 32nd + band is published;
+    // the KQ = 0 main pass never reads the union)
+    if (m_est >= 32 * BN && m_est * 8 <= h->ntotal) {
+      if ((rc = h->glock.ensure((size_t)nq * sizeof(unsigned int))) || (rc = h->gkeys.ensure((size_t)nq * 32 * 4)))
+        return rc;
+      CK(cudaMemsetAsync(h->glock.p, 0, (size_t)nq * sizeof(unsigned int), st));
+      CK(cudaMemsetAsync(h->gkeys.p, 0xFF, (size_t)nq * 32 * 4, st));
+      if ((rc = run_bound_pass(h, nq, m_est, 32, 32, 32, ip, kmode, st, true))) return rc;
+    }
   }
   rc = run_fused(h, pl, nq, h->ntotal, kp, ip, st);
   h->r_kfinal = 0;
@@ -942,7 +961,7 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
   int* fail = static_cast<int*>(h->rfail.p);
   // the filter pass's exactness flags and rounding-band coefficient (L2; IP half)
   const unsigned int* inexact = kmode == 5 ? h->inexact + 2 : (h->split == 2 ? h->inexact : nullptr);
-  const float band_l2 = kmode == 5 ? 0.0078125f : 0.015625f;
+  const float band_l2 = f1p_band(kmode);
   if (ip)
     merge_rescore_kernel<true><<<(unsigned)nq, 256, msmem, st>>>(pk, pp, pc, pl.S_tot, (int)nq, kp, k, thr, q0, q1, xb, xl, qn,
                                                                   h->norms, h->xn_max, h->dp, h->ids, dD, dI, dP, smc,
@@ -971,8 +990,14 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
         omax = std::max<long long>(omax, c);
       }
     }
-    fprintf(stderr, "[fk] mode%d k=%d k'=%d nq=%lld uncertified=%d overflow rows=%lld entries=%lld max=%lld\n", kmode,
-            k, kp, (long long)nq, nf, orows, osum, omax);
+    std::vector<int> fv(nq);
+    CK(cudaMemcpy(fv.data(), fail, nq * sizeof(int), cudaMemcpyDeviceToHost));
+    int why[5] = {0, 0, 0, 0, 0};
+    for (int v : fv) why[std::max(0, std::min(4, v))]++;
+    fprintf(stderr,
+            "[fk] mode%d k=%d k'=%d nq=%lld uncertified=%d (smem %d, band %d, <k %d, flag %d) overflow rows=%lld "
+            "entries=%lld max=%lld\n",
+            kmode, k, kp, (long long)nq, nf, why[1], why[2], why[3], why[4], orows, osum, omax);
   }
   // uncertified queries: exact fallback on the device (no host sync); up to
   // one wave of CTAs, each scanning the base for its failed queries, with a

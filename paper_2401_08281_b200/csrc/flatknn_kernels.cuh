@@ -347,8 +347,10 @@ __global__ void __launch_bounds__(256) merge_rescore_kernel(
   const int tid = threadIdx.x;
   if (q >= nq) return;
   // uncertified queries are appended to fail_list for fallback_kernel (no host round trip)
-  auto mark_failed = [&]() {
-    fail[q] = 1;
+  // fail[q]: 0 certified; reason otherwise (1 survivors > smem buffer, 2 bound
+  // does not clear the band, 3 fewer than k under the bound, 4 row flag)
+  auto mark_failed = [&](int why) {
+    fail[q] = why;
     fail_list[atomicAdd(fail_count, 1)] = q;
   };
   const uint32_t thr = thr_key[q];
@@ -385,19 +387,20 @@ __global__ void __launch_bounds__(256) merge_rescore_kernel(
   __syncthreads();
   int n = count;
   if (n > smc) {  // more survivors than the buffer: exact fallback for this query
-    if (tid == 0) mark_failed();
+    if (tid == 0) mark_failed(1);
     return;
   }
   // certification on the tf32 values
   const float qn = qnorm[q];
-  // band 2e with a 2x safety factor: L2 2 * 2 * 2^-8 (tf32 filter; band_l2 =
-  // 2^-6) or 2 * 2 * 2^-9 (scaled fp16 filter; 2^-7) times |q| max|x|, IP half;
-  // plus the fp32 accumulation slack (4 dp + 8) 2^-23 (qn + max xn)
-  // (same bound as the fused kernel's band4)
+  // band = 2 x the filter-value error bound, times |q| max|x| (band_l2 =
+  // 2^-7 tf32 / 2^-8 scaled fp16, with a 2^-10 margin; IP half), plus the fp32
+  // accumulation slack (4 dp + 8) 2^-23 (qn + max xn) (same as the fused
+  // kernel's band4)
   const bool tf32_exact = inexact != nullptr && (inexact[0] | inexact[1]) == 0u;
   const float e2 = (tf32_exact ? 0.f : (IS_IP ? 0.5f * band_l2 : band_l2)) * sqrtf(fmaxf(qn, 0.f) * fmaxf(*xn_max, 0.f)) +
                    (4.f * (float)dp + 8.f) * 1.1920928955078125e-07f * (fmaxf(qn, 0.f) + fmaxf(*xn_max, 0.f));
   bool ok = true;
+  int why = 0;
   uint32_t band_key = 0xFFFFFFFFu;  // only entries with t <= t_k + band can be in the exact top-k
   if (n >= k) {
     const uint64_t kth = block_kth([&](int e) { return sm[e]; }, n, (uint32_t)k, hist, sel);
@@ -408,15 +411,22 @@ __global__ void __launch_bounds__(256) merge_rescore_kernel(
     // every entry that did not reach a list has t >= thr, so thr must clear
     // the band.  (Register-queue lists filter with (own k-th + band) bounds,
     // which never drop a band member: only the row flag below matters.)
-    if (lc != nullptr && thr != 0xFFFFFFFFu) ok = unmonotone(thr) > lim;
+    if (lc != nullptr && thr != 0xFFFFFFFFu && !(unmonotone(thr) > lim)) {
+      ok = false;
+      why = 2;
+    }
   } else if (thr != 0xFFFFFFFFu) {
     ok = false;  // fewer than k gathered although entries were dropped
+    why = 3;
   }
   // a register queue that dropped a band member flagged its row
-  if (rflag[q]) ok = false;
+  if (rflag[q]) {
+    ok = false;
+    why = 4;
+  }
   if (tid == 0) {
     if (ok) fail[q] = 0;
-    else mark_failed();
+    else mark_failed(why);
   }
   if (!ok) return;
   // keep the band only (typically k + a few): in-place compaction

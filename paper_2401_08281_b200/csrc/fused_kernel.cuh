@@ -101,6 +101,7 @@ struct SearchParams {
   // (device scalar); NaN marks an unusable scale (row -> exact fallback)
   const float* qinv;
   const float* xinv;
+  float band_l2;  // F1P rounding-band coefficient of |q| max|x| (L2; IP half)
   int pub_mask;  // publish the own bound / fetch the shared one every pub_mask+1 own tiles
   // MODE 4: per-query running union of the finished units' best k' tf32 keys
   // (lock-protected), so the shared bound tightens towards the global k-th
@@ -697,11 +698,14 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       // merge_rescore_kernel); the bound we filter and publish with is
       // (own kfinal-th t) + band >= (global kfinal-th t) + band
       const bool tf32_exact = p.inexact != nullptr && (p.inexact[0] | p.inexact[1]) == 0u;
-      // rounding term: tf32 (raw fp32 truncated to 11 bits): |t - ip| <= 2^-9 |q||x|;
-      // scaled fp16 (RNE, 11 bits): <= (2^-10 + 2^-27) |q||x| -> half the band
-      constexpr float BAND_L2 = (MODE == 5) ? 0.0078125f : 0.015625f;
+      // rounding term (host-chosen p.band_l2, IP half): one filter pass errs
+      // by |t - ip| <= (2^-10 + 2^-20) |q||x| (tf32 truncation) or
+      // (2^-10 + 2^-27) |q||x| (RNE scaled fp16, incl. subnormals), so the
+      // filter value xn - 2t by twice that, and a true top-k member lies within
+      // 2x of it above the k-th filter value: band = 2^-7 / 2^-8 |q| max|x|
+      // (+ 2^-10 margin)
       const float band4 = (F1P && KQ > 0 && !RANGE && row_ok)
-                              ? (tf32_exact ? 0.f : (IS_IP ? 0.5f * BAND_L2 : BAND_L2)) *
+                              ? (tf32_exact ? 0.f : (IS_IP ? 0.5f * p.band_l2 : p.band_l2)) *
                                         sqrtf(fmaxf(p.qnorm[row], 0.f) * fmaxf(*p.xn_max, 0.f)) +
                                     // fp32 accumulation: the tensor core (possibly truncating,
                                     // <= dp 2^-23) and the sequential-FMA rescoring (<= dp 2^-24)

@@ -201,3 +201,31 @@ def test_filter16_large_k(metric, k, nb):
     want_ids, want_dist = O.flat_search_blas(xb, q, k, metric)
     assert_parity(r5.ids, r5.distances, want_ids, want_dist)
     assert np.array_equal(r5.ids, r4.ids) and np.array_equal(r5.distances, r4.distances)
+
+
+@pytest.mark.parametrize("filt", [None, "tf32"])
+def test_filter16_coherent_rounding_worst_case(filt):
+    """Adversarial rounding: every coordinate of the query and of row A sits
+    just below an fp16 / tf32 rounding midpoint, so the filter underestimates
+    <q, A> coherently by ~2^-10 |q||A| per pair, while 300 decoy rows are
+    exactly representable with a filter value ABOVE A's but a true inner
+    product below it.  A must survive the band (through the overflow lists:
+    the decoys fill every queue) and win after the exact rescoring."""
+    d = 64
+    a = 2.0 ** -11 - 2.0 ** -20           # q_i = x_A,i = 1 + a: rounds down to 1 in fp16 and tf32
+    q = np.full((24, d), 1 + a, dtype=np.float32)
+    x_a = np.full((1, d), 1 + a, dtype=np.float32)
+    rng = np.random.default_rng(5)
+    decoys = np.ones((300, d), dtype=np.float32)
+    for r in range(300):                  # 31 coordinates at 1 + 2^-10: mean 1 + (2^-11 - 2^-16) < 1 + a
+        decoys[r, rng.choice(d, 31, replace=False)] = 1 + 2.0 ** -10
+    filler = rng.standard_normal((300_000, d)).astype(np.float32) * 0.01
+    xb = np.vstack([filler[:150_000], decoys, x_a, filler[150_000:]])
+    a_pos = 150_000 + 300
+    idx = _index(d, "ip")
+    idx.add(xb)
+    res = _search(idx, q, 1, filt=filt)
+    assert np.all(res.ids[:, 0] == a_pos), res.ids[:, 0]
+    want_ids, want_dist = O.flat_search_blas(xb, q, 1, "ip")
+    assert np.all(want_ids[:, 0] == a_pos)
+    assert_parity(res.ids, res.distances, want_ids, want_dist)
