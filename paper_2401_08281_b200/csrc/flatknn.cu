@@ -522,21 +522,27 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   //    (an even count, see below), so A goes to smem (SS MMA) when it fits;
   //  * A in TMEM (TS MMA) beside >= 2 x 128 accumulator columns;
   //  * a large A (up to 384 TMEM columns, e.g. d=768 16-bit) stays in TMEM
-  //    with 64-column tiles (2 x 64 accumulators) rather than re-streaming A;
+  //    next to ONE 128-column accumulator: the MMA waits only for each tile's
+  //    TMEM readout (~0.2k cycles per 3k-cycle d=768 tile) -- measured 3.5 %
+  //    faster than 2 x 64-column accumulators (N=64 MMAs run at 71 %), and
+  //    half the partial lists (FK_BN=64 keeps the old plan);
   //  * otherwise A in smem, or streamed with every stage (a_mode 2).
   P.bn = 128;
+  bool single_acc = getenv("FK_ACC") && atoi(getenv("FK_ACC")) == 1;
   if (h16 && P.nh == 2 && a_bytes <= 64 * 1024) P.a_mode = 1;
   else if (kmode == 4 && a_bytes <= 64 * 1024) P.a_mode = 1;  // 1-pass fp32: 4 accumulators (+2.5 %)
   else if (a_tmem_cols <= 256) P.a_mode = 0;
   else if (a_tmem_cols <= 384) {
     P.a_mode = 0;
-    P.bn = 64;
+    single_acc = true;
   } else P.a_mode = 1;
   if (const char* e = getenv("FK_FORCE_AMODE")) P.a_mode = std::max(0, std::min(2, atoi(e)));
-  if (const char* e = getenv("FK_BN")) P.bn = atoi(e) == 64 ? 64 : 128;
-  // single accumulator (FK_ACC=1): A may take up to 512 - TBN columns; the
-  // MMA then waits for each tile's readout (one issuer, one epilogue group)
-  const bool single_acc = getenv("FK_ACC") && atoi(getenv("FK_ACC")) == 1;
+  if (const char* e = getenv("FK_BN")) {
+    P.bn = atoi(e) == 64 ? 64 : 128;
+    if (P.bn == 64 && !(getenv("FK_ACC") && atoi(getenv("FK_ACC")) == 1)) single_acc = false;
+  }
+  // single accumulator: A may take up to 512 - TBN columns; the MMA then
+  // waits for each tile's readout (one issuer, one epilogue group)
   if (P.a_mode == 0 && a_tmem_cols > 512 - (single_acc ? 1 : 2) * P.bn) P.a_mode = 1;
   if (P.a_mode != 0) P.bn = 128;
   if (P.bn == 64) {  // 64-column kernels exist only for the default epilogue width
@@ -595,6 +601,7 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   // TMEM: 512 columns = acc_stages x 128-column accumulators (+ the query operand in a_mode 0)
   P.acc_stages = std::min(4, (512 - (P.a_mode == 0 ? a_tmem_cols : 0)) / bn);
   if (const char* e = getenv("FK_ACC")) P.acc_stages = std::max(1, std::min(P.acc_stages, atoi(e)));
+  if (single_acc) P.acc_stages = 1;
   P.n_issuers = P.stages >= 4 ? 2 : 1;  // each issuer needs a sub-ring of >= 2 slots
   if (const char* e = getenv("FK_ISSUERS")) P.n_issuers = (atoi(e) == 1 || P.stages < 4) ? 1 : 2;
   // Tiles alternate between the 2 MMA issuers and between the NH epilogue

@@ -296,14 +296,17 @@ __global__ void __launch_bounds__(256) merge_large_kernel(const uint32_t* __rest
   }
 }
 
-// ------------------------------------------------------------ MODE 4 rescoring merge
-// Exact fp32 inner product over dp (sequential FMA, the order of an fp32 dot
-// product); the operands are hi (+ lo when the storage is split: hi + lo == x
-// exactly in fp32).
-__device__ __forceinline__ float exact_dot(const float4* __restrict__ qh, const float4* __restrict__ ql,
-                                           const float4* __restrict__ xh, const float4* __restrict__ xl, int dp) {
+// ------------------------------------------------------------ 1-pass rescoring merge
+// Exact fp32 inner product of one (query, row) pair by a whole warp: lane l
+// accumulates the float4 chunks l, l+32, ... sequentially (hi + lo == the fp32
+// value exactly), then a fixed xor-butterfly sums the lanes -- the same value
+// on every lane, the same summation order in the rescoring merge and the exact
+// fallback (one load round instead of dp/4 dependent ones per pair).
+__device__ __forceinline__ float warp_exact_dot(const float4* __restrict__ qh, const float4* __restrict__ ql,
+                                                const float4* __restrict__ xh, const float4* __restrict__ xl, int dp,
+                                                int lane) {
   float acc = 0.f;
-  for (int c = 0; c < dp / 4; ++c) {
+  for (int c = lane; c < dp / 4; c += 32) {
     float4 a = __ldg(qh + c), b = __ldg(xh + c);
     if (ql) {
       const float4 t = __ldg(ql + c);
@@ -318,8 +321,11 @@ __device__ __forceinline__ float exact_dot(const float4* __restrict__ qh, const 
     acc = fmaf(a.z, b.z, acc);
     acc = fmaf(a.w, b.w, acc);
   }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, off);
   return acc;
 }
+
 // fp32 MODE 4 runs the fused pass with a 1-pass TF32 GEMM and keeps k' >= k
 // entries per list ranked by their tf32 value t.  With e = max|t - v| over all
 // pairs (|t - v| <= 2^-8 |q| max|x| for L2, half for IP), every exact top-k
@@ -452,16 +458,18 @@ __global__ void __launch_bounds__(256) merge_rescore_kernel(
   // exact values for the remaining entries
   const float4* qv = reinterpret_cast<const float4*>(q0 + (size_t)q * dp);
   const float4* qlv = q1 ? reinterpret_cast<const float4*>(q1 + (size_t)q * dp) : nullptr;
-  for (int i = tid; i < n; i += blockDim.x) {
+  for (int i = tid >> 5; i < n; i += blockDim.x >> 5) {  // a warp per entry
     const uint32_t ps = static_cast<uint32_t>(sm[i]);
-    const float acc = exact_dot(qv, qlv, reinterpret_cast<const float4*>(xb + (size_t)ps * dp),
-                                xl ? reinterpret_cast<const float4*>(xl + (size_t)ps * dp) : nullptr, dp);
+    const float acc = warp_exact_dot(qv, qlv, reinterpret_cast<const float4*>(xb + (size_t)ps * dp),
+                                     xl ? reinterpret_cast<const float4*>(xl + (size_t)ps * dp) : nullptr, dp,
+                                     tid & 31);
     float v = acc;
     if (!IS_IP) {
       v = fmaf(-2.f, acc, qn + xnorm[ps]);  // flat.py:111
       v = (v <= 0.f) ? 0.f : v;              // flat.py:112
     }
-    sm[i] = (static_cast<uint64_t>(dist_key(v, IS_IP)) << 32) | ps;
+    __syncwarp();
+    if ((tid & 31) == 0) sm[i] = (static_cast<uint64_t>(dist_key(v, IS_IP)) << 32) | ps;
   }
   __syncthreads();
   uint64_t* win = sm + smc;
@@ -593,15 +601,16 @@ __global__ void __launch_bounds__(256) fallback_kernel(const int* __restrict__ f
     const float qn = qnorm[q];
     const float4* qh = reinterpret_cast<const float4*>(q0 + (size_t)q * dp);
     const float4* ql = q1 ? reinterpret_cast<const float4*>(q1 + (size_t)q * dp) : nullptr;
-    for (int64_t r = tid; r < n; r += blockDim.x) {
-      const float acc = exact_dot(qh, ql, reinterpret_cast<const float4*>(xb + (size_t)r * dp),
-                                  xl ? reinterpret_cast<const float4*>(xl + (size_t)r * dp) : nullptr, dp);
+    for (int64_t r = tid >> 5; r < n; r += blockDim.x >> 5) {  // a warp per row (same order as the merge)
+      const float acc = warp_exact_dot(qh, ql, reinterpret_cast<const float4*>(xb + (size_t)r * dp),
+                                       xl ? reinterpret_cast<const float4*>(xl + (size_t)r * dp) : nullptr, dp,
+                                       tid & 31);
       float v = acc;
       if (!IS_IP) {
         v = fmaf(-2.f, acc, qn + xnorm[r]);
         v = (v <= 0.f) ? 0.f : v;
       }
-      comp[r] = (static_cast<uint64_t>(dist_key(v, IS_IP)) << 32) | static_cast<uint32_t>(r);
+      if ((tid & 31) == 0) comp[r] = (static_cast<uint64_t>(dist_key(v, IS_IP)) << 32) | static_cast<uint32_t>(r);
     }
     block_select_write<IS_IP>(comp, (int)n, k, q, win, &count, hist, sel, ids, D, I, P);
     __syncthreads();

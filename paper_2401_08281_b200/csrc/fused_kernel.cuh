@@ -631,6 +631,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     const int a_cols = (MODE == 0) ? 2 * dp : (MODE == 4 ? dp : dp / 2);  // TMEM columns of the query operand
     uint32_t tcount = 0, a_buf = 0, a_ph = 0;
     uint32_t xs0 = 0, xp0 = 0, xs1 = 0, xp1 = 0;  // norm sub-ring positions (ring = tile % n_issuers)
+    const uint32_t xn_s_a = smem_u32(xn_s);
     const uint32_t xh = (uint32_t)xn_slots / (uint32_t)p.n_issuers;
     int uj = 0;  // units processed by this CTA
     for (int u = ublock; u < p.num_units; u += ugrid, ++uj) {
@@ -808,7 +809,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         if (tr) p.trace[tcount * 16 + 6] = clock64();
         const int n0 = t * BN;
         const int nvalid = p.nb - n0;
-        const float* xs = xn_s + xslot * BN;
+        const uint32_t xs_a = xn_s_a + xslot * (BN * 4u);  // this tile's base norms (shared address)
         // Filter on f = xn - 2 ip (L2; one FMA) or -ip (IP) against T; the
         // exact reference value (qn + xn) - 2 ip is computed for survivors only.
         auto chunk_f = [&](const uint32_t (&r)[32], int c0, float (&f)[32]) {
@@ -826,7 +827,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
               f[4 * j4 + 3] = __uint_as_float(r[4 * j4 + 3]);
             } else {
               // c2 = -2 (MODE 5: -2 * 2^-(s_q + s_x), so c2 * acc is exactly -2 t)
-              const float4 x = lds_f4(xs + c0 + 4 * j4);
+              const float4 x = lds_f4_at(xs_a + (uint32_t)(c0 + 4 * j4) * 4u);
               f[4 * j4 + 0] = fmaf(c2, __uint_as_float(r[4 * j4 + 0]), x.x);
               f[4 * j4 + 1] = fmaf(c2, __uint_as_float(r[4 * j4 + 1]), x.y);
               f[4 * j4 + 2] = fmaf(c2, __uint_as_float(r[4 * j4 + 2]), x.z);
@@ -869,7 +870,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             float v;
             if (IS_IP) v = -ip;
             else if (FOLD) v = qn + ip;
-            else v = fmaf(-2.f, ip, qn + lds_f32(xs + c0 + j));
+            else v = fmaf(-2.f, ip, qn + lds_f32_at(xs_a + (uint32_t)(c0 + j) * 4u));
             if (!(v > thr)) {
               if (!IS_IP) v = (v <= 0.f) ? 0.f : v;  // np.maximum(dmat, 0) (flat.py:112)
               const uint32_t kv = IS_IP ? dist_key(ip, true) : dist_key(v, false);

@@ -413,3 +413,28 @@ def test_large_k_estimate_fails_certification_and_reruns():
     res = idx.search(q, 200)
     want_ids, want_dist = O.flat_search_blas(xb, q, 200, "l2")
     assert_parity(res.ids, res.distances, want_ids, want_dist)
+
+
+@pytest.mark.parametrize("k", [10, 100])
+def test_large_query_operand_tile_plans(k):
+    """d = 768 16-bit (cfg4 shape): the query operand takes 384 TMEM columns;
+    the default plan keeps ONE 128-column accumulator next to it, FK_BN=64 the
+    round-1 plan of two 64-column accumulators -- identical answers, and the
+    oracle's on the rounded inputs."""
+    rng = np.random.default_rng(768)
+    xb = rng.standard_normal((30000, 768), dtype=np.float32)
+    q = rng.standard_normal((200, 768), dtype=np.float32)
+    idx = FlatIndex(768, METRIC_IP, storage="fp16")
+    idx.add(xb)
+    base = idx.search(q, k)
+    assert idx.last_plan()["bn"] == 128 and idx.last_plan()["acc_stages"] == 1
+    os.environ["FK_BN"] = "64"
+    try:
+        alt = idx.search(q, k)
+        assert idx.last_plan()["bn"] == 64
+    finally:
+        del os.environ["FK_BN"]
+    assert np.array_equal(base.ids, alt.ids) and np.array_equal(base.distances, alt.distances)
+    xr, qr = O.round_to(xb, "fp16"), O.round_to(q, "fp16")
+    want_ids, want_dist = O.flat_search_blas(xr, qr, k, "ip")
+    assert_parity(base.ids, base.distances, want_ids, want_dist)
