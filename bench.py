@@ -286,7 +286,7 @@ def run_ours(args, cfg):
         local_index = index
     else:
         from paper_2401_08281_b200.sharded import shard_range
-        index = ShardedFlatIndex(d, metric, storage=cfg["storage"], device=local)
+        index = ShardedFlatIndex(d, metric, storage=cfg["storage"], device=local, exchange=args.exchange)
         lo, hi = shard_range(nb, rank, world)
         if nb <= 2_000_000:
             index.add_local_shard(torch.from_numpy(gen_base(cfg, lo, hi)).cuda(), lo, nb)
@@ -402,8 +402,9 @@ def run_ours(args, cfg):
                    "storage": cfg["storage"],
                    "l2_flush": "inputs larger than L2: base hi+lo %.2f GB vs 126 MB L2" % (
                        nb_local * d * elem * (2 if cfg["storage"] == "fp32" else 1) / 1e9),
-                   "parallelism": f"database rows sharded over {world} GPU(s), queries replicated, "
-                                  "NCCL all-gather + merge kernel" if world > 1 else "1 GPU",
+                   "parallelism": (f"database rows sharded over {world} GPU(s), queries replicated, "
+                                   + ("NCCL all-gather + merge kernel" if args.exchange == "nccl" else
+                                      "peer-memory merge kernel (CUDA IPC / NVLink P2P)")) if world > 1 else "1 GPU",
                    "plan": plan},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": tc_peak, "unit": "TFLOP/s",
                      "frac": achieved / tc_peak, "traffic": traffic, "traffic_source": traffic_src,
@@ -496,6 +497,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+                    help="N>1: NCCL all-gather + merge kernel, or the peer-memory exchange (fk_xchg_*)")
     ap.add_argument("--dry-run", action="store_true", help="rank plumbing only (gloo, no GPU)")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -20,7 +20,7 @@
  *   FlatIndex._positions (id -> pos)   flat.py:34-41      fk_positions
  *   refine_search re-ranking           core.py:368-394    fk_refine
  *   _kernels function table errors     _kernels/__init__.py:37-41 -> fk_last_error
- *   (none: SPEC.md:115 non-goal)       SURVEY 8(e)        fk_merge_shards
+ *   (none: SPEC.md:115 non-goal)       SURVEY 8(e)        fk_merge_shards, fk_xchg_*
  *
  * Conventions: plain pointers and sizes only.  Every entry point returns 0 on
  * success or a negative FK_E* code; fk_last_error() then returns a message
@@ -89,6 +89,26 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
  * pointers are device pointers on the current device. */
 int fk_merge_shards(int metric, int nshard, int64_t nq, int k, const float* D_in, const int64_t* P_in,
                     const int64_t* I_in, float* D_out, int64_t* I_out, void* stream);
+
+/* Peer-memory exchange for the row-sharded index (the fused alternative to
+ * NCCL all-gather + fk_merge_shards).  Every rank exports one
+ * device block (CUDA IPC handle of fk_xchg_handle_bytes() bytes) holding its
+ * per-search lists and two counters; after fk_xchg_connect with every rank's
+ * handle, a search is: fk_xchg_acquire (wait until the peers finished reading
+ * this rank's previous lists) -> local search -> fk_xchg_put (distances,
+ * GLOBAL positions, ids) -> fk_xchg_merge (publish, wait for every peer,
+ * merge by (distance, global position) reading the peers' lists directly ->
+ * the single-index answer on every rank).  All on `stream`, no host sync;
+ * bounded device waits, fk_xchg_status reports a timeout. */
+typedef struct fk_xchg fk_xchg;
+int fk_xchg_handle_bytes(void);
+int fk_xchg_create(int device, int rank, int world, int64_t nq_cap, int k_cap, fk_xchg** out, void* handle_out);
+int fk_xchg_connect(fk_xchg* x, const void* all_handles);
+int fk_xchg_acquire(fk_xchg* x, void* stream);
+int fk_xchg_put(fk_xchg* x, int64_t nq, int k, const float* D, const int64_t* P, const int64_t* I, void* stream);
+int fk_xchg_merge(fk_xchg* x, int metric, int64_t nq, int k, float* D_out, int64_t* I_out, void* stream);
+int fk_xchg_status(fk_xchg* x);
+void fk_xchg_destroy(fk_xchg* x);
 
 /* Copy the stored vectors of the given storage positions back as float32
  * (flat.py:43-44 reconstruct_batch; the Python mirror maps ids->positions). */

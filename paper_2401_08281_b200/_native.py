@@ -30,6 +30,8 @@ EXPORTED = (
     "fk_set_profiling", "fk_kernel_times", "fk_last_plan", "fk_kmeans_rescore",
     "fk_range_search", "fk_range_fetch", "fk_range_total", "fk_range_free", "fk_set_option",
     "fk_positions", "fk_refine", "fk_gate",
+    "fk_xchg_handle_bytes", "fk_xchg_create", "fk_xchg_connect", "fk_xchg_acquire", "fk_xchg_put",
+    "fk_xchg_merge", "fk_xchg_status", "fk_xchg_destroy",
 )
 
 FK_OPT_PLAN_ROWS = 1
@@ -64,6 +66,14 @@ _SIGS = {
     "fk_range_free": (None, [_P]),
     "fk_set_option": (_INT, [_P, _INT, _I64]),
     "fk_gate": (_INT, [_P, ctypes.c_double, _P]),
+    "fk_xchg_handle_bytes": (_INT, []),
+    "fk_xchg_create": (_INT, [_INT, _INT, _INT, _I64, _INT, ctypes.POINTER(_P), _P]),
+    "fk_xchg_connect": (_INT, [_P, _P]),
+    "fk_xchg_acquire": (_INT, [_P, _P]),
+    "fk_xchg_put": (_INT, [_P, _I64, _INT, _P, _P, _P, _P]),
+    "fk_xchg_merge": (_INT, [_P, _INT, _I64, _INT, _P, _P, _P]),
+    "fk_xchg_status": (_INT, [_P]),
+    "fk_xchg_destroy": (None, [_P]),
     "fk_positions": (_INT, [_P, _P, _I64, _P, _INT, _P]),
     "fk_refine": (_INT, [_P, _INT, _P, _I64, _P, _INT, _INT, _P, _P, _INT, _P]),
     "fk_kmeans_rescore": (_INT, [_P, _I64, _INT, _P, _P, _I64, _P, _INT, _INT, _P, ctypes.c_double,

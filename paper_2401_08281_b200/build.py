@@ -26,7 +26,7 @@ DEV_LIB_PATH = os.path.join(PKG_DIR, "libflatknn_dev.so")
 # one translation unit per fused-kernel operand MODE (the template
 # instantiations dominate compile time) + the host/ABI unit; compiled in
 # parallel, linked into one shared library
-SOURCES = ["flatknn.cu"] + [f"fused_m{m}.cu" for m in range(6)]
+SOURCES = ["flatknn.cu", "xchg.cu"] + [f"fused_m{m}.cu" for m in range(6)]
 DEPS = SOURCES + ["flatknn_kernels.cuh", "fused_kernel.cuh", "fused_launch.cuh", "fk_host.cuh", "sm100.cuh", "storage_kernels.cuh", "filter16_kernels.cuh"]
 
 

@@ -490,7 +490,8 @@ int fk_add(fk_index* h, const void* x, int64_t n, int dtype, const int64_t* ids,
 namespace {
 
 struct Plan {
-  int kq, epi, nh, num_m, n_tiles, S, chunk_tiles, num_units, grid, a_mode, stages, smem, S_tot, cap, xn_slots,
+  int kq, epi, nh, num_m, n_tiles, S, chunk_tiles, probe_tiles, num_units, grid, a_mode, stages, smem, S_tot, cap,
+      xn_slots,
       acc_stages, n_issuers, cluster, num_mu, bn, kmode;
 };
 
@@ -577,6 +578,19 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
     P.S = std::max(1, std::min(fs, std::min(max_S, P.n_tiles)));
     P.chunk_tiles = (P.n_tiles + P.S - 1) / P.S;
     P.S = (P.n_tiles + P.chunk_tiles - 1) / P.chunk_tiles;
+  }
+  // Probe chunk (register-queue lists): a short chunk 0 per query tile lets the
+  // first units finish early and publish the running-union bound while the
+  // long chunks are still in their insertion-heavy start (FK_PROBE = tiles)
+  P.probe_tiles = 0;
+  {
+    int probe = 0;
+    if (const char* e = getenv("FK_PROBE")) probe = std::max(0, atoi(e));
+    if (probe > 0 && kq > 0 && P.S >= 2 && P.n_tiles > 4 * probe) {
+      P.probe_tiles = probe;
+      P.chunk_tiles = (P.n_tiles - probe + P.S - 1) / P.S;
+      P.S = 1 + (P.n_tiles - probe + P.chunk_tiles - 1) / P.chunk_tiles;
+    }
   }
   P.num_units = P.num_mu * P.S;  // per CTA pair in cluster mode
   P.grid = P.cluster * std::min(P.num_units, h->num_sms / P.cluster);
@@ -669,6 +683,7 @@ int run_fused(fk_index* h, const Plan& P, int64_t nq, int64_t nb_pass, int k, bo
   sp.num_m = P.num_m;
   sp.n_tiles = P.n_tiles;
   sp.chunk_tiles = P.chunk_tiles;
+  sp.probe_tiles = P.probe_tiles;
   sp.S = P.S;
   sp.num_units = P.num_units;
   sp.num_kb = dpk / (h16 ? 64 : 32);

@@ -76,6 +76,7 @@ struct SearchParams {
   const void* qa1;     // lo part (fp32 mode)
   int nq, nb, k;
   int num_m, n_tiles, chunk_tiles, S, num_units;
+  int probe_tiles;  // > 0: chunk 0 is a short probe chunk [0, probe_tiles), the others follow it
   int num_kb;      // padded d / elements-per-128B-chunk
   int a_mode;      // 0: queries in TMEM, 1: resident in smem, 2: streamed per stage
   int stages;      // B (and streamed A) pipeline depth
@@ -125,6 +126,20 @@ struct SearchParams {
   int dbg_flags;   // bottleneck experiments (FK_DEBUG_FLAGS): 1 = epilogue skips TMEM loads + compute,
                    // 2 = producer skips TMA, 4 = no slow path, 8 = TMEM loads without the filter
 };
+
+// Base tiles [t0, t1) of N-chunk `chunk`.  With a probe chunk, chunk 0 is
+// short so the first units of every query finish early and publish a bound
+// (the running union) before the long chunks have inserted much.
+__device__ __forceinline__ void chunk_range(const SearchParams& p, int chunk, int& t0, int& t1) {
+  if (p.probe_tiles > 0) {
+    t0 = chunk == 0 ? 0 : p.probe_tiles + (chunk - 1) * p.chunk_tiles;
+    t1 = chunk == 0 ? p.probe_tiles : t0 + p.chunk_tiles;
+  } else {
+    t0 = chunk * p.chunk_tiles;
+    t1 = t0 + p.chunk_tiles;
+  }
+  t1 = min(t1, p.n_tiles);
+}
 
 // ------------------------------------------------------------ register queue
 // Sorted ascending (worst at KQ-1).  Slots [0, KQ-k) hold phantom key 0 which
@@ -449,8 +464,8 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       for (int u = ublock; u < p.num_units; u += ugrid, ++j) {
         const int chunk = u / p.num_mu;
         const int m = (u - chunk * p.num_mu) * CL + (int)crank;
-        const int t0 = chunk * p.chunk_tiles;
-        const int t1 = min(t0 + p.chunk_tiles, p.n_tiles);
+        int t0, t1;
+        chunk_range(p, chunk, t0, t1);
         if (a_mode == 1 && myring == 0) {
           if (j > 0) mbar_wait(aempty, (j - 1) & 1);
           mbar_arrive_expect_tx(afull, a_bytes);
@@ -528,8 +543,8 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       const int kk_last = p.kk_last;
       for (int u = ublock; u < p.num_units; u += ugrid, ++j) {
         const int chunk = u / p.num_mu;
-        const int t0 = chunk * p.chunk_tiles;
-        const int t1 = min(t0 + p.chunk_tiles, p.n_tiles);
+        int t0, t1;
+        chunk_range(p, chunk, t0, t1);
         if (a_mode != 2) {
           mbar_wait(afull, j & 1);
           tc_fence_after();
@@ -637,8 +652,8 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     for (int u = ublock; u < p.num_units; u += ugrid, ++uj) {
       const int chunk = u / p.num_mu;
       const int m = (u - chunk * p.num_mu) * CL + (int)crank;
-      const int t0 = chunk * p.chunk_tiles;
-      const int t1 = min(t0 + p.chunk_tiles, p.n_tiles);
+      int t0, t1;
+      chunk_range(p, chunk, t0, t1);
       const int row = m * BM + eq * 32 + lane;
       const bool row_ok = row < p.nq;
 
@@ -961,6 +976,8 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
                 atomicAdd(reinterpret_cast<unsigned long long*>(p.trace + 256 * 16 + 0), 1ull);  // warp-pieces
                 if (sbl) atomicAdd(reinterpret_cast<unsigned long long*>(p.trace + 256 * 16 + 1), 1ull);
                 atomicAdd(reinterpret_cast<unsigned long long*>(p.trace + 256 * 16 + 2), (unsigned long long)__popc(sbl));
+                // slow warp-pieces by chunk (slots 3..14: chunks 0..11; and by wave: units < grid)
+                if (sbl) atomicAdd(reinterpret_cast<unsigned long long*>(p.trace + 256 * 16 + 3 + min(chunk, 11)), 1ull);
               }
             }
             if (slow) {  // divergent, rare

@@ -8,6 +8,11 @@ replicated; each rank runs the fused GEMM + top-k over its shard and returns
 the union by (distance, global position) -- exactly the unsharded reference
 order (flat.py:94-118 + core.py:205-236 on the concatenated database).
 
+``exchange="p2p"`` replaces the all-gather + merge by the peer-memory
+exchange (``fk_xchg_*``): every rank's merge kernel reads the other ranks'
+lists directly over NVLink P2P (CUDA IPC), with device-side ready/done
+counters instead of a collective or a host synchronisation.
+
 The reference has no distributed search (SPEC.md:115 lists distributed result
 merging as a non-goal); parity here means: sharded result == single-index
 result on the same data.
@@ -58,7 +63,7 @@ class ShardedFlatIndex:
     """
 
     def __init__(self, d: int, metric: Metric = METRIC_L2, storage: str = "fp32", group=None, device=None,
-                 local_factory=None, merge_fn=None):
+                 local_factory=None, merge_fn=None, exchange: str = "nccl"):
         if dist is None or not dist.is_initialized():
             raise RuntimeError("ShardedFlatIndex needs an initialised torch.distributed process group")
         self.group = group
@@ -73,6 +78,11 @@ class ShardedFlatIndex:
             local_factory = FlatIndex
         self.local = local_factory(d, metric, storage, device)
         self.merge_fn = merge_fn or native_merge
+        if exchange not in ("nccl", "p2p"):
+            raise ValueError("exchange must be 'nccl' or 'p2p'")
+        self.exchange = exchange
+        self._xchg = None
+        self._xcap = (0, 0)
         self.ntotal = 0
         self.is_trained = True
         self._gpos_parts: list = []
@@ -159,6 +169,8 @@ class ShardedFlatIndex:
         if k < 1:
             raise ValueError("k must be >= 1")
         q = as_vectors(q, self.d)
+        if self.exchange == "p2p":
+            return self._search_p2p(q, int(k))
         res, P = self.local.search_with_positions(q, int(k))
         D, I = res.distances, res.ids
         if not is_torch(D):
@@ -187,3 +199,76 @@ class ShardedFlatIndex:
         parts = [torch.empty_like(t) for _ in range(self.world)]
         dist.all_gather(parts, t, group=self.group)
         return torch.stack(parts)
+
+    # ------------------------------------------------------------------ peer-memory exchange
+    def _global_positions(self, P):
+        table = self._gpos_table(P)
+        if table.numel():
+            return torch.where(P >= 0, table[P.clamp(min=0)], torch.full_like(P, -1))
+        return torch.full_like(P, -1)
+
+    def _xchg_ensure(self, nq: int, k: int, device: int):
+        """(Re)create the exchange when the result shape outgrows it -- every
+        rank sees the same (nq, k) (queries are replicated), so all ranks do
+        this collectively: handles are exchanged with all_gather_object."""
+        from . import _native as N
+        import ctypes
+        if self._xchg is not None and nq <= self._xcap[0] and k <= self._xcap[1]:
+            return self._xchg
+        L = N.lib()
+        self._xchg_close()
+        cap = (max(nq, self._xcap[0]), max(k, self._xcap[1]))
+        hb = L.fk_xchg_handle_bytes()
+        handle = (ctypes.c_char * hb)()
+        x = ctypes.c_void_p()
+        N.check(L.fk_xchg_create(device, self.rank, self.world, cap[0], cap[1], ctypes.byref(x), handle))
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(handle), group=self.group)
+        allh = (ctypes.c_char * (hb * self.world)).from_buffer_copy(b"".join(handles))
+        N.check(L.fk_xchg_connect(x, allh))
+        self._xchg, self._xcap = x, cap
+        return x
+
+    def _xchg_close(self):
+        if self._xchg is not None:
+            from . import _native as N
+            torch.cuda.synchronize()
+            dist.barrier(group=self.group)  # no peer still reads this rank's block
+            N.lib().fk_xchg_destroy(self._xchg)
+            self._xchg = None
+
+    def xchg_status(self) -> None:
+        """Synchronise and raise if a device-side exchange wait timed out."""
+        if self._xchg is not None:
+            from . import _native as N
+            N.check(N.lib().fk_xchg_status(self._xchg))
+
+    def _search_p2p(self, q, k: int) -> SearchResult:
+        from . import _native as N
+        host = not (is_torch(q) and q.is_cuda)
+        dev = self.local.device
+        qd = q.to(f"cuda:{dev}") if is_torch(q) else torch.from_numpy(np.ascontiguousarray(q)).to(f"cuda:{dev}")
+        res, P = self.local.search_with_positions(qd, k)
+        nq = qd.shape[0]
+        Pg = self._global_positions(P).contiguous()
+        x = self._xchg_ensure(nq, k, dev)
+        L = N.lib()
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        Dm = torch.empty((nq, k), dtype=torch.float32, device=qd.device)
+        Im = torch.empty((nq, k), dtype=torch.int64, device=qd.device)
+        code = N.FK_METRIC_IP if self._mv == "ip" else N.FK_METRIC_L2
+        N.check(L.fk_xchg_acquire(x, stream))
+        N.check(L.fk_xchg_put(x, nq, k, res.distances.data_ptr(), Pg.data_ptr(), res.ids.data_ptr(), stream))
+        N.check(L.fk_xchg_merge(x, code, nq, k, Dm.data_ptr(), Im.data_ptr(), stream))
+        if host:
+            return SearchResult(Im.cpu().numpy(), Dm.cpu().numpy(), k)
+        return SearchResult(Im, Dm, k)
+
+    def __del__(self):
+        try:
+            if self._xchg is not None:
+                from . import _native as N
+                N.lib().fk_xchg_destroy(self._xchg)
+                self._xchg = None
+        except Exception:
+            pass

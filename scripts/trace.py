@@ -43,5 +43,6 @@ print("epilogue group 0: LDTM piece0 latency", m(t[ev, 11] - t[ev, 2]), "| piece
       "| piece1 compute + tail", m(t[ev, 7] - t[ev, 12]), "| got tfull -> ld issue", m(t[ev, 2] - t[ev, 6]))
 slow = t[:, 8]
 print("slow-path lanes per tile (warp 4): mean", slow[sl].mean(), "tiles with any", (slow[sl] > 0).mean())
+print("slow warp-pieces by chunk 0..11:", list(t_all[256, 3:15]))
 print("ALL CTAs: warp-pieces", t_all[256, 0], "with slow path", t_all[256, 1],
       f"({t_all[256, 1] / max(t_all[256, 0], 1):.4f})", "slow lanes", t_all[256, 2])
