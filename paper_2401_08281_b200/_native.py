@@ -92,6 +92,9 @@ def lib() -> ctypes.CDLL:
     global _lib
     if _lib is None:
         path = DEV_LIB_PATH if os.environ.get("FK_DEV_LIB") == "1" else LIB_PATH
+        if os.environ.get("FK_LIB_VARIANT"):  # experiment builds (scripts only)
+            from .build import variant_path
+            path = variant_path(os.environ["FK_LIB_VARIANT"])
         if not os.path.exists(path):
             raise ImportError(
                 f"{path} is missing: the CUDA extension is not built "

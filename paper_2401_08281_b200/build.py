@@ -45,8 +45,15 @@ def needs_build(path: str = LIB_PATH) -> bool:
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 
 
-def build(force: bool = False, verbose: bool = True, dev: bool = False) -> str:
-    out = DEV_LIB_PATH if dev else LIB_PATH
+def variant_path(name: str) -> str:
+    return os.path.join(PKG_DIR, f"libflatknn_{name}.so")
+
+
+def build(force: bool = False, verbose: bool = True, dev: bool = False, variant: str | None = None,
+          defines: tuple = ()) -> str:
+    """variant/defines: an experiment library libflatknn_<variant>.so built with
+    extra -D flags (loaded only with FK_LIB_VARIANT=<variant>, scripts only)."""
+    out = variant_path(variant) if variant else (DEV_LIB_PATH if dev else LIB_PATH)
     if not force and not needs_build(out):
         return out
     nvcc = nvcc_path()
@@ -56,8 +63,8 @@ def build(force: bool = False, verbose: bool = True, dev: bool = False) -> str:
         "-Xcompiler", "-fPIC,-O3",
         "-Xptxas", "-v",
         "-I", os.path.join(REPO, "include"),
-    ] + (["-DFK_DEV=1"] if dev else [])
-    objdir = os.path.join(PKG_DIR, "_obj_dev" if dev else "_obj")
+    ] + (["-DFK_DEV=1"] if dev else []) + [f"-D{d}" for d in defines]
+    objdir = os.path.join(PKG_DIR, f"_obj_{variant}" if variant else ("_obj_dev" if dev else "_obj"))
     os.makedirs(objdir, exist_ok=True)
     procs = []
     for src in SOURCES:
@@ -72,7 +79,7 @@ def build(force: bool = False, verbose: bool = True, dev: bool = False) -> str:
         logs.append(f"==== {src}\n{text}")
         if pr.returncode != 0:
             failed.append(src)
-    log_path = os.path.join(PKG_DIR, "build_dev.log" if dev else "build.log")
+    log_path = os.path.join(PKG_DIR, f"build_{variant}.log" if variant else ("build_dev.log" if dev else "build.log"))
     with open(log_path, "w") as f:
         f.write("\n".join(logs))
     if failed:

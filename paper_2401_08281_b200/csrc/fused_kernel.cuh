@@ -734,14 +734,17 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       // queue slot of the caller's k-th (MODE 4 keeps k' >= kfinal entries);
       // read through a static select so the queue stays in registers
       const int kf_slot = (KQS - k) + p.kfinal - 1;
+      // F1P: (kfinal-th filter key + band), cached -- it only changes when an
+      // insertion lands at or before the kfinal-th slot
+      auto band_bound = [&](uint32_t kk) -> uint32_t {
+        if (kk == 0xFFFFFFFFu) return kk;
+        const float b = unmonotone(kk) + band4;
+        return (b != b) ? 0xFFFFFFFFu : monotone(b);
+      };
+      uint32_t kth_f1p = 0xFFFFFFFFu, own_f1p = 0xFFFFFFFFu;
       auto own_key = [&]() -> uint32_t {
         if constexpr (KQ > 0) {
-          if (F1P) {
-            const uint32_t kk = select_static<KQS>(keys, kf_slot);
-            if (kk == 0xFFFFFFFFu) return kk;
-            const float b = unmonotone(kk) + band4;
-            return (b != b) ? 0xFFFFFFFFu : monotone(b);
-          }
+          if (F1P) return own_f1p;
           return keys[KQS - 1];
         }
         return lkey;
@@ -901,6 +904,12 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
                   }
                 }
                 queue_insert<KQS>(keys, pos, kv, static_cast<uint32_t>(n0 + c0 + j));
+                if (F1P) {
+                  if (kv < kth_f1p) {  // the kfinal-th slot moved
+                    kth_f1p = select_static<KQS>(keys, kf_slot);
+                    own_f1p = band_bound(kth_f1p);
+                  }
+                }
                 const uint32_t bk = min(own_key(), gkey);
                 thr = unmonotone(bk);
                 T = filter_bound(thr);

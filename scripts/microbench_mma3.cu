@@ -150,7 +150,7 @@ void runp(unsigned long long* d) {
 // each, own sub-rings), accumulator ring of NACC buffers (tfull commit per
 // tile), NG epilogue groups of 4 warps alternate tiles: wait tfull ->
 // (optionally LDTM the tile) -> arrive tempty.  SS: A from smem.
-template <int NIS, bool SS, int NACC, int NG, bool LD>
+template <int NIS, bool SS, int NACC, int NG, bool LD, int BSTRIDE = 4096, bool RANDOM = false>
 __global__ void pipe2(int tiles, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -158,7 +158,18 @@ __global__ void pipe2(int tiles, unsigned long long* out) {
   __shared__ uint32_t slot;
   __shared__ uint64_t full[NS], empty[NS], tfull[NACC], tempty[NACC];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+  for (int i = threadIdx.x; i < (BSTRIDE * 8 + 32768) / 4; i += blockDim.x) {
+    uint32_t v = 0;
+    if (RANDOM) {  // two fp16 values in [-2, 2): sign, exponent 14..15, random mantissa
+      uint32_t h = (uint32_t)i * 2654435761u ^ (blockIdx.x * 40503u);
+      h ^= h >> 13;
+      h *= 0x5bd1e995u;
+      h ^= h >> 15;
+      const uint32_t lo = (h & 0x83FFu) | 0x3800u, hi = ((h >> 16) & 0x83FFu) | 0x3C00u;
+      v = lo | (hi << 16);
+    }
+    reinterpret_cast<uint32_t*>(smem)[i] = v;
+  }
   if (warp == 0) tmem_alloc(&slot, 512);
   if (threadIdx.x == 32) {
     for (int i = 0; i < NS; ++i) {
@@ -195,7 +206,7 @@ __global__ void pipe2(int tiles, unsigned long long* out) {
   } else if (warp == 1 || (warp == 3 && NIS == 2)) {
     constexpr uint32_t idesc = make_idesc(0u, 128, 128);
     const uint64_t b0 = smem_desc_sw128(smem_u32(smem));
-    const uint64_t a0 = smem_desc_sw128(smem_u32(smem + 32768));
+    const uint64_t a0 = smem_desc_sw128(smem_u32(smem + BSTRIDE * 8));
     const uint32_t mw = warp == 1 ? 0 : 1;
     uint32_t rs = 0, rph = 0, buf = 0, tph = 0;
     for (int t = 0; t < tiles; ++t) {
@@ -212,8 +223,8 @@ __global__ void pipe2(int tiles, unsigned long long* out) {
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
-            if (SS) mma_f16(tmem + cb * 128, a0 + (kb * 16384 >> 4) + 2 * kk, b0 + (s * 4096 >> 4) + 2 * kk, idesc, kb | kk);
-            else mma_f16_ts(tmem + cb * 128, tmem + 448 + 8 * kk, b0 + (s * 4096 >> 4) + 2 * kk, idesc, kb | kk);
+            if (SS) mma_f16(tmem + cb * 128, a0 + (kb * 16384 >> 4) + 2 * kk, b0 + (s * BSTRIDE >> 4) + 2 * kk, idesc, kb | kk);
+            else mma_f16_ts(tmem + cb * 128, tmem + 448 + 8 * kk, b0 + (s * BSTRIDE >> 4) + 2 * kk, idesc, kb | kk);
           }
           mma_commit(&empty[s]);
         }
@@ -258,15 +269,16 @@ __global__ void pipe2(int tiles, unsigned long long* out) {
   }
 }
 
-template <int NIS, bool SS, int NACC, int NG, bool LD>
+template <int NIS, bool SS, int NACC, int NG, bool LD, int BSTRIDE = 4096, bool RANDOM = false>
 void runp2(unsigned long long* d, int tiles = 1024) {
-  auto k = pipe2<NIS, SS, NACC, NG, LD>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 1024);
+  auto k = pipe2<NIS, SS, NACC, NG, LD, BSTRIDE, RANDOM>;
+  const int smem = BSTRIDE * 8 + 32768 + 1024;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  k<<<148, 128 + 32 * 4 * NG, 65536 + 1024>>>(tiles, d);
+  k<<<148, 128 + 32 * 4 * NG, smem>>>(tiles, d);
   cudaEventRecord(e1);
   cudaError_t e = cudaDeviceSynchronize();
   float ms = 0;
@@ -280,7 +292,7 @@ void runp2(unsigned long long* d, int tiles = 1024) {
   double c = 0;
   for (int i = 0; i < 148; ++i) c += h[i];
   c /= 148;
-  printf("pipe2 issuers %d %s acc %d groups %d ldtm %d tiles %d: %6.1f cyc/MMA  %.3f ms  %.0f MHz  %.0f TF/s\n", NIS,
+  printf("pipe2 random %d bstride %d issuers %d %s acc %d groups %d ldtm %d tiles %d: %6.1f cyc/MMA  %.3f ms  %.0f MHz  %.0f TF/s\n", (int)RANDOM, BSTRIDE, NIS,
          SS ? "SS" : "TS", NACC, NG, (int)LD, tiles, c / (tiles * 8), ms, c / (ms * 1e3),
          2.0 * 128 * 128 * 16 * 8.0 * tiles * 148 / (ms * 1e9));
 }
@@ -329,8 +341,10 @@ int main() {
   runp2<2, true, 4, 2, true>(d);
   runp2<1, false, 2, 1, true>(d);
   runp2<2, false, 2, 2, true>(d);
-  runp2<2, true, 4, 2, true>(d, 8192);
-  runp2<2, true, 4, 2, true>(d, 65536);
-  runp2<1, false, 2, 1, true>(d, 65536);
+  runp2<2, true, 4, 2, true, 16384>(d, 8192);
+  runp2<2, true, 4, 2, true, 16384, true>(d, 8192);
+  runp2<1, false, 2, 1, false, 16384>(d, 8192);
+  runp2<1, false, 2, 1, false, 16384, true>(d, 8192);
+  runp2<2, true, 4, 2, true, 16384, true>(d, 65536);
   return 0;
 }
