@@ -984,7 +984,20 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
   // the filter pass's exactness flags and rounding-band coefficient (L2; IP half)
   const unsigned int* inexact = kmode == 5 ? h->inexact + 2 : (h->split == 2 ? h->inexact : nullptr);
   const float band_l2 = f1p_band(kmode);
-  if (ip)
+  // register-queue lists of a few hundred entries per query: the
+  // warp-per-query merge (same certification, band and exact values)
+  const bool warp_merge = kq > 0 && (size_t)pl.S_tot * kp <= 1024 && k <= 32 &&
+                          !(getenv("FK_MERGE_WARP") && atoi(getenv("FK_MERGE_WARP")) == 0);
+  const auto rfl = static_cast<const unsigned int*>(h->rflag.p);
+  if (warp_merge && ip)
+    merge_rescore_warp_kernel<true><<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(
+        pk, pp, pl.S_tot, (int)nq, kp, k, thr, q0, q1, xb, xl, qn, h->norms, h->xn_max, h->dp, h->ids, dD, dI, dP,
+        fail, fcount, flist, rfl, inexact, band_l2, okey, opos, ocnt, ovf_cap);
+  else if (warp_merge)
+    merge_rescore_warp_kernel<false><<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(
+        pk, pp, pl.S_tot, (int)nq, kp, k, thr, q0, q1, xb, xl, qn, h->norms, h->xn_max, h->dp, h->ids, dD, dI, dP,
+        fail, fcount, flist, rfl, inexact, band_l2, okey, opos, ocnt, ovf_cap);
+  else if (ip)
     merge_rescore_kernel<true><<<(unsigned)nq, 256, msmem, st>>>(pk, pp, pc, pl.S_tot, (int)nq, kp, k, thr, q0, q1, xb, xl, qn,
                                                                   h->norms, h->xn_max, h->dp, h->ids, dD, dI, dP, smc,
                                                                   fail, fcount, flist,

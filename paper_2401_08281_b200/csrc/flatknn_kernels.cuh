@@ -519,6 +519,147 @@ __global__ void __launch_bounds__(256) merge_rescore_kernel(
   }
 }
 
+// Warp-per-query form of merge_rescore_kernel for register-queue lists
+// (S * k' small, k <= 32): 8 queries per CTA, the gathered composites in a
+// warp-private smem buffer (W_SMW entries; more -> exact fallback), ranks by
+// counting instead of block-wide radix selects, the same certification, band
+// and warp_exact_dot rescoring (values bit-identical to the CTA form).
+constexpr int W_SMW = 256;
+template <bool IS_IP>
+__global__ void __launch_bounds__(256) merge_rescore_warp_kernel(
+    const uint32_t* __restrict__ pkey, const uint32_t* __restrict__ ppos, int S, int nq, int kp, int k,
+    const uint32_t* __restrict__ thr_key, const float* __restrict__ q0, const float* __restrict__ q1,
+    const float* __restrict__ xb, const float* __restrict__ xl, const float* __restrict__ qnorm,
+    const float* __restrict__ xnorm, const float* __restrict__ xn_max, int dp, const int64_t* __restrict__ ids,
+    float* __restrict__ D, int64_t* __restrict__ I, int64_t* __restrict__ P, int* __restrict__ fail,
+    int* __restrict__ fail_count, int* __restrict__ fail_list, const unsigned int* __restrict__ rflag,
+    const unsigned int* __restrict__ inexact, float band_l2, const uint32_t* __restrict__ ovf_key,
+    const uint32_t* __restrict__ ovf_pos, const unsigned int* __restrict__ ovf_cnt, int ovf_cap) {
+  __shared__ uint64_t sbuf[8][W_SMW];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = blockIdx.x * 8 + w;
+  if (q >= nq) return;
+  uint64_t* buf = sbuf[w];
+  auto mark_failed = [&](int why) {
+    if (lane == 0) {
+      fail[q] = why;
+      fail_list[atomicAdd(fail_count, 1)] = q;
+    }
+  };
+  const uint32_t thr = thr_key[q];
+  const int total = S * kp;
+  int n = 0;
+  auto push = [&](bool take, uint64_t v) {
+    const unsigned b = __ballot_sync(0xFFFFFFFFu, take);
+    const int at = n + __popc(b & ((1u << lane) - 1u));
+    if (take && at < W_SMW) buf[at] = v;
+    n += __popc(b);
+  };
+  for (int e0 = 0; e0 < total; e0 += 32) {
+    const int e = e0 + lane;
+    uint64_t v = 0;
+    bool take = false;
+    if (e < total) {
+      const uint32_t key = pkey[(size_t)q * total + e];
+      const uint32_t ps = ppos[(size_t)q * total + e];
+      take = key <= thr && ps != 0xFFFFFFFFu;
+      v = (static_cast<uint64_t>(key) << 32) | ps;
+    }
+    push(take, v);
+  }
+  if (ovf_cnt != nullptr) {
+    const int no = min((int)ovf_cnt[q], ovf_cap);
+    for (int e0 = 0; e0 < no; e0 += 32) {
+      const int e = e0 + lane;
+      uint64_t v = 0;
+      bool take = false;
+      if (e < no) {
+        const uint32_t key = ovf_key[(size_t)q * ovf_cap + e];
+        take = key <= thr;
+        v = (static_cast<uint64_t>(key) << 32) | ovf_pos[(size_t)q * ovf_cap + e];
+      }
+      push(take, v);
+    }
+  }
+  __syncwarp();
+  if (n > W_SMW) {
+    mark_failed(1);
+    return;
+  }
+  // rank of buf[i] among the n (unique) composites
+  auto rank_of = [&](uint64_t v, int cnt) {
+    int r = 0;
+    for (int j = 0; j < cnt; ++j) r += buf[j] < v;
+    return r;
+  };
+  const float qn = qnorm[q];
+  const bool tf32_exact = inexact != nullptr && (inexact[0] | inexact[1]) == 0u;
+  const float e2 = (tf32_exact ? 0.f : (IS_IP ? 0.5f * band_l2 : band_l2)) * sqrtf(fmaxf(qn, 0.f) * fmaxf(*xn_max, 0.f)) +
+                   (4.f * (float)dp + 8.f) * 1.1920928955078125e-07f * (fmaxf(qn, 0.f) + fmaxf(*xn_max, 0.f));
+  uint32_t band_key = 0xFFFFFFFFu;
+  int why = 0;
+  if (n >= k) {
+    uint64_t kth = ~0ull;
+    for (int i = lane; i < n; i += 32)
+      if (rank_of(buf[i], n) == k - 1) kth = buf[i];
+    kth = warp_min_u64(kth);
+    const float tk = unmonotone(static_cast<uint32_t>(kth >> 32));
+    band_key = monotone(tk + e2 + 9.5367431640625e-07f * (fabsf(tk) + qn));
+  } else if (thr != 0xFFFFFFFFu) {
+    why = 3;
+  }
+  if (rflag[q]) why = 4;
+  if (why) {
+    mark_failed(why);
+    return;
+  }
+  if (lane == 0) fail[q] = 0;
+  // keep the band (order-preserving warp compaction), rescore exactly
+  int m = 0;
+  for (int i0 = 0; i0 < n; i0 += 32) {
+    const int i = i0 + lane;
+    const uint64_t v = i < n ? buf[i] : 0;
+    const bool keep = i < n && static_cast<uint32_t>(v >> 32) <= band_key;
+    const unsigned b = __ballot_sync(0xFFFFFFFFu, keep);
+    __syncwarp();
+    if (keep) buf[m + __popc(b & ((1u << lane) - 1u))] = v;
+    m += __popc(b);
+    __syncwarp();
+  }
+  const float4* qv = reinterpret_cast<const float4*>(q0 + (size_t)q * dp);
+  const float4* qlv = q1 ? reinterpret_cast<const float4*>(q1 + (size_t)q * dp) : nullptr;
+  for (int i = 0; i < m; ++i) {
+    const uint32_t ps = static_cast<uint32_t>(buf[i]);
+    const float acc = warp_exact_dot(qv, qlv, reinterpret_cast<const float4*>(xb + (size_t)ps * dp),
+                                     xl ? reinterpret_cast<const float4*>(xl + (size_t)ps * dp) : nullptr, dp, lane);
+    float v = acc;
+    if (!IS_IP) {
+      v = fmaf(-2.f, acc, qn + xnorm[ps]);  // flat.py:111
+      v = (v <= 0.f) ? 0.f : v;              // flat.py:112
+    }
+    __syncwarp();
+    if (lane == 0) buf[i] = (static_cast<uint64_t>(dist_key(v, IS_IP)) << 32) | ps;
+    __syncwarp();
+  }
+  // the first k by (exact key, position), best first, padded
+  for (int i = lane; i < m; i += 32) {
+    const uint64_t v = buf[i];
+    const int r = rank_of(v, m);
+    if (r < k) {
+      const size_t o = (size_t)q * k + r;
+      D[o] = key_dist(static_cast<uint32_t>(v >> 32), IS_IP);
+      I[o] = ids[static_cast<uint32_t>(v)];
+      if (P) P[o] = static_cast<uint32_t>(v);
+    }
+  }
+  for (int r = m + lane; r < k; r += 32) {
+    const size_t o = (size_t)q * k + r;
+    D[o] = IS_IP ? -INFINITY : INFINITY;
+    I[o] = -1;
+    if (P) P[o] = -1;
+  }
+}
+
 // Exact top-k of one query from its n composites (key << 32 | position):
 // block radix select of the k-th, compaction, bitonic sort of the winners,
 // then (distance, id, position) rows with -1 / worst padding.  All threads of

@@ -46,6 +46,17 @@ def _ptr(x) -> int:
     return x.data_ptr() if is_torch(x) else x.ctypes.data
 
 
+def _host_out(shape, dtype):
+    """Output array for host results: pinned (torch caching host allocator)
+    when CUDA is usable and the array is large enough to matter, else plain
+    numpy.  Either way a fresh numpy array owned by the caller."""
+    n = int(np.prod(shape))
+    if torch is not None and n * np.dtype(dtype).itemsize >= (1 << 16) and torch.cuda.is_available():
+        tdt = {np.dtype(np.float32): torch.float32, np.dtype(np.int64): torch.int64}[np.dtype(dtype)]
+        return torch.empty(shape, dtype=tdt, pin_memory=True).numpy()
+    return np.empty(shape, dtype=dtype)
+
+
 def _stream_of(device: int) -> int:
     if torch is None or not torch.cuda.is_available():
         return 0
@@ -204,9 +215,12 @@ class FlatIndex(Index):
         else:
             if is_torch(q):
                 q = q.contiguous()
-            D = np.empty((nq, k), dtype=np.float32)
-            I = np.empty((nq, k), dtype=np.int64)
-            P = np.empty((nq, k), dtype=np.int64) if with_positions else None
+            # results land in page-locked host memory (torch's caching host
+            # allocator: a recycled block after the first call) so the D2H copy
+            # runs at DMA speed; the numpy arrays keep their block alive
+            D = _host_out((nq, k), np.float32)
+            I = _host_out((nq, k), np.int64)
+            P = _host_out((nq, k), np.int64) if with_positions else None
             N.check(L.fk_search(self._h, _ptr(q), nq, _dtype_code(q), k, D.ctypes.data, I.ctypes.data,
                                 P.ctypes.data if P is not None else None, 0, 0))
         res = SearchResult(I, D, k)
