@@ -104,6 +104,12 @@ float f1p_band(int kmode) {
   return b;
 }
 
+// smallest database (global rows) served by the 1-pass path (FK_FP32_1PASS_MINROWS)
+int64_t fp32_1pass_min_rows() {
+  if (const char* e = getenv("FK_FP32_1PASS_MINROWS")) return atoll(e);
+  return FP32_1X_MIN_ROWS;
+}
+
 // largest k served by the 1-pass filter + rescoring path (FK_FP32_1PASS_MAXK)
 int fp32_1pass_max_k() {
   if (const char* e = getenv("FK_FP32_1PASS_MAXK")) return atoi(e);
@@ -1356,7 +1362,7 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
     h->plan[11] = -1;  // direct path
   } else if (h->storage == FK_F32 &&
              (h->split == 1 ||
-              (k <= fp32_1pass_max_k() && (h->plan_rows > 0 ? h->plan_rows : h->ntotal) >= FP32_1X_MIN_ROWS &&
+              (k <= fp32_1pass_max_k() && (h->plan_rows > 0 ? h->plan_rows : h->ntotal) >= fp32_1pass_min_rows() &&
                !getenv("FK_FP32_3X")))) {
     // filter pass: scaled fp16 (MODE 5, default with the hi/lo storage) or
     // tf32 (MODE 4; FK_FP32_FILTER=tf32, or raw fp32 storage)

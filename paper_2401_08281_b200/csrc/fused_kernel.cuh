@@ -587,6 +587,19 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
                     mma_tf32_ts(d_tmem, ah + 8 * kk, bd1 + off, IDESC, 1u);                        // hi*lo
                     mma_tf32_ts(d_tmem, ah + 8 * kk, bd0 + off, IDESC, 1u);                        // hi*hi
                   }
+                } else if (nkk == 4) {  // full 128-byte K-chunk: 4 MMAs, no padding checks
+                  const uint32_t acc0 = kb != 0;
+                  if (MODE == 4) {
+                    mma_tf32_ts(d_tmem, ah, bd0, IDESC, acc0);
+                    mma_tf32_ts(d_tmem, ah + 8, bd0 + 2, IDESC, 1u);
+                    mma_tf32_ts(d_tmem, ah + 16, bd0 + 4, IDESC, 1u);
+                    mma_tf32_ts(d_tmem, ah + 24, bd0 + 6, IDESC, 1u);
+                  } else {
+                    mma_f16_ts(d_tmem, ah, bd0, IDESC, acc0);
+                    mma_f16_ts(d_tmem, ah + 8, bd0 + 2, IDESC, 1u);
+                    mma_f16_ts(d_tmem, ah + 16, bd0 + 4, IDESC, 1u);
+                    mma_f16_ts(d_tmem, ah + 24, bd0 + 6, IDESC, 1u);
+                  }
                 } else {
 #pragma unroll
                   for (int kk = 0; kk < 4; ++kk) {
@@ -608,6 +621,19 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
                     mma_tf32(d_tmem, ad1 + off, bd0 + off, IDESC, (kb | kk) != 0);
                     mma_tf32(d_tmem, ad0 + off, bd1 + off, IDESC, 1u);
                     mma_tf32(d_tmem, ad0 + off, bd0 + off, IDESC, 1u);
+                  }
+                } else if (nkk == 4) {  // full 128-byte K-chunk: 4 MMAs, no padding checks
+                  const uint32_t acc0 = kb != 0;
+                  if (MODE == 4) {
+                    mma_tf32(d_tmem, ad0, bd0, IDESC, acc0);
+                    mma_tf32(d_tmem, ad0 + 2, bd0 + 2, IDESC, 1u);
+                    mma_tf32(d_tmem, ad0 + 4, bd0 + 4, IDESC, 1u);
+                    mma_tf32(d_tmem, ad0 + 6, bd0 + 6, IDESC, 1u);
+                  } else {
+                    mma_f16(d_tmem, ad0, bd0, IDESC, acc0);
+                    mma_f16(d_tmem, ad0 + 2, bd0 + 2, IDESC, 1u);
+                    mma_f16(d_tmem, ad0 + 4, bd0 + 4, IDESC, 1u);
+                    mma_f16(d_tmem, ad0 + 6, bd0 + 6, IDESC, 1u);
                   }
                 } else {
 #pragma unroll
