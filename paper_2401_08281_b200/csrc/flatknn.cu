@@ -945,7 +945,7 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
     // (the sample's units and epilogue groups each see part of it: their
     // lists merge into the per-query union, whose 32nd + band is published;
     // the KQ = 0 main pass never reads the union)
-    if (m_est >= 32 * BN && m_est * 8 <= h->ntotal) {
+    if (m_est >= 32 * BN && m_est * 4 <= h->ntotal) {
       if ((rc = h->glock.ensure((size_t)nq * sizeof(unsigned int))) || (rc = h->gkeys.ensure((size_t)nq * 32 * 4)))
         return rc;
       CK(cudaMemsetAsync(h->glock.p, 0, (size_t)nq * sizeof(unsigned int), st));
@@ -963,7 +963,7 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
   int* fcount = static_cast<int*>(h->rfail.p) + 2 * nq;  // device list of uncertified queries
   int* flist = static_cast<int*>(h->rfail.p) + nq;
   CK(cudaMemsetAsync(fcount, 0, sizeof(int), st));
-  const int smc = std::min(MERGE_SMC, std::max(1024, 8 * kp));
+  const int smc = std::min(MERGE_SMC, std::max(1024, 24 * kp));
   int p2 = 1;
   while (p2 < k) p2 <<= 1;
   static std::atomic<uint64_t> cfg{0};

@@ -326,6 +326,46 @@ __device__ __forceinline__ float warp_exact_dot(const float4* __restrict__ qh, c
   return acc;
 }
 
+// The same value as warp_exact_dot computed by ONE thread (the exact
+// fallback scans a whole base per failed query: a thread per row keeps its
+// loads in flight): the 32 lane partials in the same sequential order, then
+// the xor-butterfly's pairing (lane 0's view: v[i] += v[i + off]).
+__device__ __forceinline__ float thread_exact_dot(const float4* __restrict__ qh, const float4* __restrict__ ql,
+                                                  const float4* __restrict__ xh, const float4* __restrict__ xl,
+                                                  int dp) {
+  float v[32];
+#pragma unroll
+  for (int l = 0; l < 32; ++l) v[l] = 0.f;
+  for (int c0 = 0; c0 < dp / 4; c0 += 32) {
+#pragma unroll
+    for (int l = 0; l < 32; ++l) {
+      const int c = c0 + l;
+      if (c < dp / 4) {
+        float4 a = __ldg(qh + c), b = __ldg(xh + c);
+        if (ql) {
+          const float4 t = __ldg(ql + c);
+          a = make_float4(a.x + t.x, a.y + t.y, a.z + t.z, a.w + t.w);
+        }
+        if (xl) {
+          const float4 t = __ldg(xl + c);
+          b = make_float4(b.x + t.x, b.y + t.y, b.z + t.z, b.w + t.w);
+        }
+        float acc = v[l];
+        acc = fmaf(a.x, b.x, acc);
+        acc = fmaf(a.y, b.y, acc);
+        acc = fmaf(a.z, b.z, acc);
+        acc = fmaf(a.w, b.w, acc);
+        v[l] = acc;
+      }
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+    for (int i = 0; i < off; ++i) v[i] = v[i] + v[i + off];
+  return v[0];
+}
+
 // fp32 MODE 4 runs the fused pass with a 1-pass TF32 GEMM and keeps k' >= k
 // entries per list ranked by their tf32 value t.  With e = max|t - v| over all
 // pairs (|t - v| <= 2^-8 |q| max|x| for L2, half for IP), every exact top-k
@@ -742,16 +782,15 @@ __global__ void __launch_bounds__(256) fallback_kernel(const int* __restrict__ f
     const float qn = qnorm[q];
     const float4* qh = reinterpret_cast<const float4*>(q0 + (size_t)q * dp);
     const float4* ql = q1 ? reinterpret_cast<const float4*>(q1 + (size_t)q * dp) : nullptr;
-    for (int64_t r = tid >> 5; r < n; r += blockDim.x >> 5) {  // a warp per row (same order as the merge)
-      const float acc = warp_exact_dot(qh, ql, reinterpret_cast<const float4*>(xb + (size_t)r * dp),
-                                       xl ? reinterpret_cast<const float4*>(xl + (size_t)r * dp) : nullptr, dp,
-                                       tid & 31);
+    for (int64_t r = tid; r < n; r += blockDim.x) {  // a thread per row, the merge's summation order
+      const float acc = thread_exact_dot(qh, ql, reinterpret_cast<const float4*>(xb + (size_t)r * dp),
+                                         xl ? reinterpret_cast<const float4*>(xl + (size_t)r * dp) : nullptr, dp);
       float v = acc;
       if (!IS_IP) {
         v = fmaf(-2.f, acc, qn + xnorm[r]);
         v = (v <= 0.f) ? 0.f : v;
       }
-      if ((tid & 31) == 0) comp[r] = (static_cast<uint64_t>(dist_key(v, IS_IP)) << 32) | static_cast<uint32_t>(r);
+      comp[r] = (static_cast<uint64_t>(dist_key(v, IS_IP)) << 32) | static_cast<uint32_t>(r);
     }
     block_select_write<IS_IP>(comp, (int)n, k, q, win, &count, hist, sel, ids, D, I, P);
     __syncthreads();

@@ -25,6 +25,12 @@
 #ifndef FK_DEV
 #define FK_DEV 0
 #endif
+// experiment switch (variant builds): 1 = unrolled 4-MMA issue for full
+// K-chunks (A/B on cfg2: MMA-only 2.09 vs 2.19 ms but the full kernel 3.68 vs
+// 3.44 ms -- off)
+#ifndef FK_ISSUER_FAST
+#define FK_ISSUER_FAST 0
+#endif
 
 namespace fk {
 
@@ -587,7 +593,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
                     mma_tf32_ts(d_tmem, ah + 8 * kk, bd1 + off, IDESC, 1u);                        // hi*lo
                     mma_tf32_ts(d_tmem, ah + 8 * kk, bd0 + off, IDESC, 1u);                        // hi*hi
                   }
-                } else if (nkk == 4) {  // full 128-byte K-chunk: 4 MMAs, no padding checks
+                } else if (FK_ISSUER_FAST && nkk == 4) {  // full 128-byte K-chunk: 4 MMAs, no padding checks
                   const uint32_t acc0 = kb != 0;
                   if (MODE == 4) {
                     mma_tf32_ts(d_tmem, ah, bd0, IDESC, acc0);
@@ -622,7 +628,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
                     mma_tf32(d_tmem, ad0 + off, bd1 + off, IDESC, 1u);
                     mma_tf32(d_tmem, ad0 + off, bd0 + off, IDESC, 1u);
                   }
-                } else if (nkk == 4) {  // full 128-byte K-chunk: 4 MMAs, no padding checks
+                } else if (FK_ISSUER_FAST && nkk == 4) {  // full 128-byte K-chunk: 4 MMAs, no padding checks
                   const uint32_t acc0 = kb != 0;
                   if (MODE == 4) {
                     mma_tf32(d_tmem, ad0, bd0, IDESC, acc0);

@@ -229,3 +229,28 @@ def test_filter16_coherent_rounding_worst_case(filt):
     want_ids, want_dist = O.flat_search_blas(xb, q, 1, "ip")
     assert np.all(want_ids[:, 0] == a_pos)
     assert_parity(res.ids, res.distances, want_ids, want_dist)
+
+
+def test_filter16_fallback_values_equal_certified_values():
+    """Queries forced into the exact fallback (no overflow lists, 8-deep
+    queues) return bit-identical values and ids to the certified rescoring
+    merge: both sum the fp32 products in the same order (warp_exact_dot /
+    thread_exact_dot)."""
+    rng = np.random.default_rng(21)
+    xb = rng.standard_normal((70000, 96), dtype=np.float32)
+    q = rng.standard_normal((200, 96), dtype=np.float32)
+    idx = _index(96, "l2")
+    idx.add(xb)
+    base = idx.search(q, 10)
+    old = {n: os.environ.get(n) for n in ("FK_OVF", "FK_KP")}
+    os.environ["FK_OVF"] = "0"
+    os.environ["FK_KP"] = "10"
+    try:
+        forced = idx.search(q, 10)
+    finally:
+        for n, v in old.items():
+            if v is None:
+                os.environ.pop(n, None)
+            else:
+                os.environ[n] = v
+    assert np.array_equal(base.ids, forced.ids) and np.array_equal(base.distances, forced.distances)
