@@ -48,9 +48,9 @@ typedef struct fk_index fk_index;
 #define FK_METRIC_L2 1
 
 /* storage / input dtypes */
-#define FK_F32 0  /* storage: fp32 (k <= 16 over >= 256k rows: raw fp32 rows, one tf32 pass
-                     + certified exact fp32 rescoring; otherwise the hi/lo tf32 split and
-                     3xTF32; fp32-faithful either way) */
+#define FK_F32 0  /* storage: fp32 as an exact tf32 hi/lo split (k <= 16, or 33 <~ k <= 128,
+                     over >= 256k rows: one scaled-fp16 filter pass + certified exact fp32
+                     rescoring; otherwise 3xTF32; fp32-faithful either way) */
 #define FK_F16 1  /* storage: fp16 (RNE from f32), tensor-core kind::f16      */
 #define FK_BF16 2 /* storage: bf16 (RNE from f32), tensor-core kind::f16      */
 

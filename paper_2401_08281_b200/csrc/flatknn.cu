@@ -113,7 +113,24 @@ int64_t fp32_1pass_min_rows() {
 // largest k served by the 1-pass filter + rescoring path (FK_FP32_1PASS_MAXK)
 int fp32_1pass_max_k() {
   if (const char* e = getenv("FK_FP32_1PASS_MAXK")) return atoi(e);
-  return 16;
+  return 128;
+}
+// sample rows of the large-k bound pass (the 32nd of 8 ntotal / k rows sits
+// near the 4k-th overall); 0 when it would cost more than a quarter pass
+int64_t est_rows(int64_t rows, int k) {
+  const int64_t m = ((rows * 8) / k + BN - 1) / BN * BN;
+  return (m >= 32 * BN && m * 4 <= rows) ? m : 0;
+}
+// 1-pass filter + rescoring for fp32 storage: k <= 16 (register queues), or
+// 16 < k <= FK_FP32_1PASS_MAXK when the sampled bound pass is affordable
+// (measured on 1M x 128, 10k queries: k = 64 6.9 vs 12.0 ms 3xTF32, k = 100
+// 6.8 vs 11.2; without the bound pass k = 32 loses, 11.7 vs 10.0; k = 1024
+// loses to the rescoring gather, 31 vs 12.8)
+// rows: the global row count (plan rows of a shard), local: this index's
+// own rows (where the bound pass samples)
+bool fp32_1pass_ok(int k, int64_t rows, int64_t local) {
+  if (rows < fp32_1pass_min_rows() || k > fp32_1pass_max_k()) return false;
+  return k <= 16 || est_rows(local, k) > 0;
 }
 int elem_bytes_of(int storage) { return storage == FK_F32 ? 4 : 2; }
 int chunk_elems_of(int storage) { return storage == FK_F32 ? 32 : 64; }
@@ -941,11 +958,11 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
     // m = 8 ntotal / k rows) + band -- near the 4k-th overall for unordered
     // data -- so the lists the merge gathers stay ~4k deep; the merge
     // certifies bound > t_k + band per query (else the exact fallback)
-    int64_t m_est = ((h->ntotal * 8) / k + BN - 1) / BN * BN;
+    const int64_t m_est = est_rows(h->ntotal, k);
     // (the sample's units and epilogue groups each see part of it: their
     // lists merge into the per-query union, whose 32nd + band is published;
     // the KQ = 0 main pass never reads the union)
-    if (m_est >= 32 * BN && m_est * 4 <= h->ntotal) {
+    if (m_est > 0) {
       if ((rc = h->glock.ensure((size_t)nq * sizeof(unsigned int))) || (rc = h->gkeys.ensure((size_t)nq * 32 * 4)))
         return rc;
       CK(cudaMemsetAsync(h->glock.p, 0, (size_t)nq * sizeof(unsigned int), st));
@@ -1362,7 +1379,7 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
     h->plan[11] = -1;  // direct path
   } else if (h->storage == FK_F32 &&
              (h->split == 1 ||
-              (k <= fp32_1pass_max_k() && (h->plan_rows > 0 ? h->plan_rows : h->ntotal) >= fp32_1pass_min_rows() &&
+              (fp32_1pass_ok(k, h->plan_rows > 0 ? h->plan_rows : h->ntotal, h->ntotal) &&
                !getenv("FK_FP32_3X")))) {
     // filter pass: scaled fp16 (MODE 5, default with the hi/lo storage) or
     // tf32 (MODE 4; FK_FP32_FILTER=tf32, or raw fp32 storage)

@@ -176,7 +176,7 @@ def test_filter16_inf_rows_and_nan_query():
 
 
 @pytest.mark.parametrize("metric", ["l2", "ip"])
-@pytest.mark.parametrize("k,nb", [(32, 80_000), (100, 80_000), (1024, 600_000)])
+@pytest.mark.parametrize("k,nb", [(40, 80_000), (100, 80_000), (1024, 600_000)])
 def test_filter16_large_k(metric, k, nb):
     """k > 16 through the 1-pass filter (FK_FP32_1PASS_MAXK): large-k
     candidate lists (KQ = 0), the sampled bound pass (600k rows, k = 1024)
@@ -254,3 +254,28 @@ def test_filter16_fallback_values_equal_certified_values():
             else:
                 os.environ[n] = v
     assert np.array_equal(base.ids, forced.ids) and np.array_equal(base.distances, forced.distances)
+
+
+@pytest.mark.parametrize("metric", ["l2", "ip"])
+@pytest.mark.parametrize("k", [24, 40, 64, 128])
+def test_filter16_mid_k_default_path(metric, k):
+    """16 < k <= 128 on a database large enough for the sampled bound pass
+    (k >= ~33 here) takes the 1-pass path by default (k = 24 keeps 3xTF32):
+    same answers as the oracle and as the forced 3xTF32 path."""
+    rng = np.random.default_rng(900 + k)
+    xb = rng.standard_normal((400_000, 32), dtype=np.float32)
+    q = rng.standard_normal((96, 32), dtype=np.float32)
+    from paper_2401_08281_b200 import METRIC_IP, METRIC_L2, FlatIndex
+    idx = FlatIndex(32, METRIC_IP if metric == "ip" else METRIC_L2, storage="fp32")
+    idx.add(xb)
+    res = idx.search(q, k)
+    assert idx.last_plan()["kmode"] == (0 if k == 24 else 5)
+    want_ids, want_dist = O.flat_search_blas(xb, q, k, metric)
+    assert_parity(res.ids, res.distances, want_ids, want_dist)
+    os.environ["FK_FP32_3X"] = "1"
+    try:
+        r3 = idx.search(q, k)
+        assert idx.last_plan()["kmode"] == 0
+    finally:
+        del os.environ["FK_FP32_3X"]
+    assert_parity(res.ids, res.distances, r3.ids, r3.distances)
