@@ -382,6 +382,9 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  // debug timeline window (FK_DEV): tiles [TOFF, TOFF + 256) of CTA 0, epilogue lane quarter TQ
+  const uint32_t TOFF = FK_DEV ? (uint32_t)(p.dbg_flags >> 20) * 256u : 0u;
+  const int TQ = FK_DEV ? (p.dbg_flags >> 16) & 3 : 0;
   const int num_kb = p.num_kb;
   const int stages = p.stages;
   const int a_mode = p.a_mode;
@@ -562,11 +565,11 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             tph ^= 1;
           }
           if (nis == 2 && (tcount & 1) != mw) continue;
-          const bool tr = FK_DEV && p.trace != nullptr && blockIdx.x == 0 && tcount < 256 && lane == 0;
-          if (tr) p.trace[tcount * 16 + 0] = clock64();
+          const bool tr = FK_DEV && p.trace != nullptr && blockIdx.x == 0 && tcount - TOFF < 256u && lane == 0;
+          if (tr) p.trace[(tcount - TOFF) * 16 + 0] = clock64();
           mbar_wait(&tempty[cbuf], cph ^ 1);
           tc_fence_after();
-          if (tr) p.trace[tcount * 16 + 1] = clock64();
+          if (tr) p.trace[(tcount - TOFF) * 16 + 1] = clock64();
           const uint32_t d_tmem = tmem_base + cbuf * BN;
           for (int kb = 0; kb < num_kb; ++kb) {
             const int nkk = (kb == num_kb - 1) ? kk_last : 4;  // skip all-zero K padding steps
@@ -577,7 +580,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             }
             mbar_wait(&full[stage], phase);
             tc_fence_after();
-            if (tr && kb < 4) p.trace[tcount * 16 + 13 + (kb < 3 ? kb : 2)] = clock64();
+            if (tr && kb < 4) p.trace[(tcount - TOFF) * 16 + 13 + (kb < 3 ? kb : 2)] = clock64();
             // descriptor start address is in 16-byte units (bits 0-13)
             const uint64_t bd0 = st_desc0 + ((stage * stage_bytes) >> 4);
             const uint64_t bd1 = bd0 + (B_CHUNK >> 4);
@@ -654,11 +657,11 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
               else mma_commit(&empty[stage]);
             }
             __syncwarp();
-            if (tr && kb < 4) p.trace[tcount * 16 + 9 + kb] = clock64();
+            if (tr && kb < 4) p.trace[(tcount - TOFF) * 16 + 9 + kb] = clock64();
           }
           if (elect_one()) mma_commit(&tfull[cbuf]);
           __syncwarp();
-          if (tr) p.trace[tcount * 16 + 3] = clock64();
+          if (tr) p.trace[(tcount - TOFF) * 16 + 3] = clock64();
         }
         if (a_mode != 2) {  // the unit's MMAs retired: A may be replaced (smem: producer, TMEM: epilogue)
           if (elect_one()) mma_commit(aempty);
@@ -850,13 +853,13 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
           }
         }
         if (NG > 1 && (tcount & (NG - 1)) != (uint32_t)g) continue;  // another group's tile
-        const bool tr = FK_DEV && p.trace != nullptr && blockIdx.x == 0 && tcount < 256 && eq == 0 && lane == 0;
-        if (tr) p.trace[tcount * 16 + 4] = clock64();
+        const bool tr = FK_DEV && p.trace != nullptr && blockIdx.x == 0 && tcount - TOFF < 256u && eq == TQ && lane == 0;
+        if (tr) p.trace[(tcount - TOFF) * 16 + 4] = clock64();
         mbar_wait(&tfull[buf], tph);
-        if (tr) p.trace[tcount * 16 + 5] = clock64();
+        if (tr) p.trace[(tcount - TOFF) * 16 + 5] = clock64();
         if (XN_TILE) mbar_wait(&xfull[xslot], xph);
         tc_fence_after();
-        if (tr) p.trace[tcount * 16 + 6] = clock64();
+        if (tr) p.trace[(tcount - TOFF) * 16 + 6] = clock64();
         const int n0 = t * BN;
         const int nvalid = p.nb - n0;
         const uint32_t xs_a = xn_s_a + xslot * (BN * 4u);  // this tile's base norms (shared address)
@@ -974,7 +977,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
 #pragma unroll
         for (int pc = 0; pc < BN / PIECE; ++pc) {
           uint32_t racc[PIECE];
-          if (tr && pc == 0) p.trace[tcount * 16 + 2] = clock64();
+          if (tr && pc == 0) p.trace[(tcount - TOFF) * 16 + 2] = clock64();
           if (do_epi) {
 #pragma unroll
             for (int c = 0; c < PIECE / 32; ++c)
@@ -982,7 +985,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
                                  *reinterpret_cast<uint32_t(*)[32]>(&racc[32 * c]));
             tmem_ld_wait();
           }
-          if (tr && pc < 2) p.trace[tcount * 16 + 11 + pc] = clock64();
+          if (tr && pc < 2) p.trace[(tcount - TOFF) * 16 + 11 + pc] = clock64();
           if (pc == BN / PIECE - 1) {
             tc_fence_before();
             __syncwarp();
@@ -1009,9 +1012,9 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             const bool slow = !(m > T) && row_ok && !(p.dbg_flags & 4);
             if (FK_DEV && p.trace != nullptr) {
               const unsigned sb = __ballot_sync(FULLMASK, slow);
-              if (tr) p.trace[tcount * 16 + 8] += __popc(sb);
+              if (tr) p.trace[(tcount - TOFF) * 16 + 8] += __popc(sb);
             }
-            if (FK_DEV && p.trace != nullptr) {  // slow-path statistics over all CTAs (trace row 256)
+            if (FK_DEV && p.trace != nullptr && !(p.dbg_flags & 0x8000)) {  // slow-path statistics over all CTAs (trace row 256; 0x8000: off)
               const unsigned sbl = __ballot_sync(FULLMASK, slow);
               if (lane == 0) {
                 atomicAdd(reinterpret_cast<unsigned long long*>(p.trace + 256 * 16 + 0), 1ull);  // warp-pieces
@@ -1033,7 +1036,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
           }
         }
         __syncwarp();
-        if (tr) p.trace[tcount * 16 + 7] = clock64();
+        if (tr) p.trace[(tcount - TOFF) * 16 + 7] = clock64();
         if (lane == 0 && XN_TILE) mbar_arrive(&xempty[xslot]);
         if (!RANGE && (++own_tiles & p.pub_mask) == 0 && row_ok) {  // publish own k-th, fetch the shared bound
           const uint32_t mine = own_key();
