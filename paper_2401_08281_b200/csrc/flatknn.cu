@@ -770,7 +770,11 @@ int launch_merge(fk_index* h, const Plan& P, int64_t nq, int k, bool ip, float* 
     // survivors buffer sized to the expected survivor count (~k..2k, the
     // radix-select fallback covers overflow) so several CTAs share an SM;
     // winners: k padded to a power of two for the bitonic sort
-    int smc = std::min(MERGE_SMC, std::max(1024, 4 * k));
+    // k >= 512 (S lists of k each: ~S*k/2 survivors): an 8k-entry buffer and
+    // 512 threads per query (cfg3 k=1024: merge 2.07 -> 1.33 ms; smaller k:
+    // 4k entries and 256 threads stay best, cfg4 k=100)
+    const bool big_k = k >= 512;
+    int smc = std::min(MERGE_SMC, std::max(1024, (big_k ? 8 : 4) * k));
     if (const char* e = getenv("FK_MERGE_SMC")) smc = std::max(1, std::min(MERGE_SMC, atoi(e)));
     int p2 = 1;
     while (p2 < k) p2 <<= 1;
@@ -786,12 +790,14 @@ int launch_merge(fk_index* h, const Plan& P, int64_t nq, int k, bool ip, float* 
     if (rc) return rc;
     const int* pc = P.kq == 0 ? static_cast<const int*>(h->pcnt.p) : nullptr;  // queue lists: k entries each
     const uint32_t* thr = static_cast<const uint32_t*>(h->thr.p);
+    int mthreads = big_k ? 512 : 256;
+    if (const char* e = getenv("FK_MERGE_THREADS")) mthreads = std::max(32, std::min(1024, atoi(e))) / 32 * 32;
     if (ip)
-      merge_large_kernel<true><<<(unsigned)nq, 256, msmem, st>>>(pk, pp, pc, P.S_tot, (int)nq, k, thr, h->ids, dD, dI,
-                                                                  dP, smc, fail);
+      merge_large_kernel<true><<<(unsigned)nq, mthreads, msmem, st>>>(pk, pp, pc, P.S_tot, (int)nq, k, thr, h->ids, dD,
+                                                                       dI, dP, smc, fail);
     else
-      merge_large_kernel<false><<<(unsigned)nq, 256, msmem, st>>>(pk, pp, pc, P.S_tot, (int)nq, k, thr, h->ids, dD,
-                                                                   dI, dP, smc, fail);
+      merge_large_kernel<false><<<(unsigned)nq, mthreads, msmem, st>>>(pk, pp, pc, P.S_tot, (int)nq, k, thr, h->ids,
+                                                                        dD, dI, dP, smc, fail);
   } else {
     const int wpb = 8;
     const unsigned mgrid = (unsigned)((nq + wpb - 1) / wpb);

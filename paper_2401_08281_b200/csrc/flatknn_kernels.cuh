@@ -179,7 +179,7 @@ __device__ uint64_t block_kth(Load load, int n, uint32_t k, uint32_t* hist, uint
 // finds the k-th (key, position); the k winners are bitonic-sorted.  If the
 // survivors overflow smem the select reads the lists from global instead.
 template <bool IS_IP>
-__global__ void __launch_bounds__(256) merge_large_kernel(const uint32_t* __restrict__ pkey,
+__global__ void __launch_bounds__(1024) merge_large_kernel(const uint32_t* __restrict__ pkey,
                                                           const uint32_t* __restrict__ ppos,
                                                           const int* __restrict__ pcnt, int S, int nq, int k,
                                                           const uint32_t* __restrict__ thr_key,

@@ -35,7 +35,8 @@ def to_bytes(v, unit):
 
 
 traffic = {}
-for rep, name in ((f"full_{tag}.ncu-rep", "cfg2"), (f"full5_{tag}.ncu-rep", "cfg5_2M")):
+for rep, name in ((f"full_{tag}.ncu-rep", "cfg2"), (f"full2_{tag}.ncu-rep", "cfg2"), (f"full3_{tag}.ncu-rep", "cfg3"),
+                  (f"full4_{tag}.ncu-rep", "cfg4_2M"), (f"full5_{tag}.ncu-rep", "cfg5_2M")):
     p = os.path.join(reps, rep)
     if not os.path.exists(p):
         continue
@@ -48,14 +49,21 @@ for rep, name in ((f"full_{tag}.ncu-rep", "cfg2"), (f"full5_{tag}.ncu-rep", "cfg
     wr = to_bytes(r["dram__bytes_write.sum"], u["dram__bytes_write.sum"])
     traffic[name] = {"kernel": r["Kernel Name"], "dram_read_bytes": rd, "dram_write_bytes": wr,
                      "traffic_bytes": rd + wr, "duration_ms": float(r["gpu__time_duration.sum"].replace(",", "")),
-                     "capture": f"profiles/{tag}/ncu_full_fused_{name}.txt"}
+                     "capture": os.path.relpath(os.path.join(dst, f"ncu_full_fused_{name}.txt"), REPO)}
 print("summaries ->", dst)
-for f in (f"launches_{tag}.csv", f"bench_{tag}.json", f"sweep_{tag}.jsonl"):
+for c in range(1, 6):  # per-config bench lines of the evidence pass (last JSON line of each)
+    b = os.path.join(src, f"bench_{tag}_cfg{c}.json")
+    if os.path.exists(b):
+        lines = [l for l in open(b) if l.startswith("{")]
+        if lines:
+            with open(os.path.join(dst, f"bench_cfg{c}.json"), "w") as f:
+                f.write(lines[-1])
+for f in (f"launches_{tag}.csv", f"bench_{tag}.json", f"sweep_{tag}.jsonl", f"pytest_{tag}.log"):
     if os.path.exists(os.path.join(src, f)):
         shutil.copy(os.path.join(src, f), os.path.join(dst, f))
 with open(os.path.join(dst, "ncu_traffic.json"), "w") as f:
     json.dump(traffic, f, indent=1)
-if traffic and "--out" not in sys.argv:
+if traffic and ("--out" not in sys.argv or "--global" in sys.argv):
     with open(os.path.join(REPO, "profiles", "ncu_traffic.json"), "w") as f:
         json.dump(dict(traffic, tag=tag), f, indent=1)
 print(json.dumps(traffic, indent=1))
