@@ -513,6 +513,7 @@ int fk_add(fk_index* h, const void* x, int64_t n, int dtype, const int64_t* ids,
 namespace {
 
 struct Plan {
+  int a_kt = 0;  // a_mode 3: K-chunks of the query operand kept in TMEM
   int kq, epi, nh, num_m, n_tiles, S, chunk_tiles, probe_tiles, num_units, grid, a_mode, stages, smem, S_tot, cap,
       xn_slots,
       acc_stages, n_issuers, cluster, num_mu, bn, kmode;
@@ -545,11 +546,13 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   //  * 16-bit with two epilogue groups: the accumulator ring wants 4 buffers
   //    (an even count, see below), so A goes to smem (SS MMA) when it fits;
   //  * A in TMEM (TS MMA) beside >= 2 x 128 accumulator columns;
-  //  * a large A (up to 384 TMEM columns, e.g. d=768 16-bit) stays in TMEM
-  //    next to ONE 128-column accumulator: the MMA waits only for each tile's
-  //    TMEM readout (~0.2k cycles per 3k-cycle d=768 tile) -- measured 3.5 %
-  //    faster than 2 x 64-column accumulators (N=64 MMAs run at 71 %), and
-  //    half the partial lists (FK_BN=64 keeps the old plan);
+  //  * a large 16-bit A (257-384 TMEM columns, e.g. d=768) is split (a_mode
+  //    3): its first 8 K-chunks (256 columns) in TMEM beside TWO 128-column
+  //    accumulators, the rest resident in smem (SS MMAs for those K-steps);
+  //    one accumulator would drain the MMA pipe at every tile (cfg4 shape:
+  //    MMA-only 118 cycles per MMA).  FK_AMODE3=0: the old plan (A wholly in
+  //    TMEM beside ONE accumulator, 3.5 % faster than 2 x 64-column
+  //    accumulators; FK_BN=64 keeps that one);
   //  * otherwise A in smem, or streamed with every stage (a_mode 2).
   P.bn = 128;
   bool single_acc = getenv("FK_ACC") && atoi(getenv("FK_ACC")) == 1;
@@ -557,9 +560,21 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   else if (kmode == 4 && a_bytes <= 64 * 1024) P.a_mode = 1;  // 1-pass fp32: 4 accumulators (+2.5 %)
   else if (a_tmem_cols <= 256) P.a_mode = 0;
   else if (a_tmem_cols <= 384) {
-    P.a_mode = 0;
-    single_acc = true;
+    if (h16 && !(getenv("FK_AMODE3") && atoi(getenv("FK_AMODE3")) == 0) && !getenv("FK_BN")) {
+      P.a_mode = 3;
+      P.a_kt = 8;  // 8 x 32 TMEM columns (64 16-bit K per chunk)
+    } else {
+      P.a_mode = 0;
+      single_acc = true;
+    }
   } else P.a_mode = 1;
+  // split operand: ONE epilogue group keeps up with the d = 768 MMA (cfg4
+  // shape: 28.2 vs 31.0 ms with two, and half the partial lists); range
+  // search keeps the default width
+  if (P.a_mode == 3 && kq >= 0 && !getenv("FK_EPI")) {
+    P.epi = 4;
+    P.nh = 1;
+  }
   if (const char* e = getenv("FK_FORCE_AMODE")) P.a_mode = std::max(0, std::min(2, atoi(e)));
   if (const char* e = getenv("FK_BN")) {
     P.bn = atoi(e) == 64 ? 64 : 128;
@@ -623,8 +638,11 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   P.xn_slots = (h->metric == FK_METRIC_IP || h->fold) ? 0 : (!h16 && P.a_mode != 2) ? 4 : 8;
   const int xn_bytes = P.xn_slots * bn * 4;
   auto stage_bytes_for = [&](int mode) { return split * b_chunk + (mode == 2 ? split * (int)CHUNK_BYTES : 0); };
+  // smem-resident query chunks: all (a_mode 1) or those past the TMEM part (a_mode 3)
+  const int a_tail_bytes = split * (num_kb - P.a_kt) * (int)CHUNK_BYTES;
+  auto a_smem_for = [&](int mode) { return mode == 1 ? a_bytes : (mode == 3 ? a_tail_bytes : 0); };
   auto stages_for = [&](int mode) {
-    const int avail = SMEM_LIMIT - SMEM_RESERVE - hist_bytes - xn_bytes - (mode == 1 ? a_bytes : 0);
+    const int avail = SMEM_LIMIT - SMEM_RESERVE - hist_bytes - xn_bytes - a_smem_for(mode);
     return avail / stage_bytes_for(mode);
   };
   P.stages = stages_for(P.a_mode);
@@ -636,7 +654,7 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   if (const char* e = getenv("FK_STAGES")) P.stages = std::max(2, std::min(P.stages, atoi(e)));
   if (P.stages < 2) return set_err(FK_E_UNSUPPORTED, "pipeline does not fit in shared memory");
   // TMEM: 512 columns = acc_stages x 128-column accumulators (+ the query operand in a_mode 0)
-  P.acc_stages = std::min(4, (512 - (P.a_mode == 0 ? a_tmem_cols : 0)) / bn);
+  P.acc_stages = std::min(4, (512 - (P.a_mode == 0 ? a_tmem_cols : (P.a_mode == 3 ? P.a_kt * 32 : 0))) / bn);
   if (const char* e = getenv("FK_ACC")) P.acc_stages = std::max(1, std::min(P.acc_stages, atoi(e)));
   if (single_acc) P.acc_stages = 1;
   P.n_issuers = P.stages >= 4 ? 2 : 1;  // each issuer needs a sub-ring of >= 2 slots
@@ -651,7 +669,7 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
     P.nh = 1;
   }
   if ((P.n_issuers == 2 || P.nh == 2) && (P.acc_stages & 1)) P.acc_stages -= 1;
-  P.smem = SMEM_RESERVE + hist_bytes + xn_bytes + (P.a_mode == 1 ? a_bytes : 0) + P.stages * stage_bytes_for(P.a_mode);
+  P.smem = SMEM_RESERVE + hist_bytes + xn_bytes + a_smem_for(P.a_mode) + P.stages * stage_bytes_for(P.a_mode);
   P.S_tot = P.S * P.nh;
   P.cap = kq == 0 ? (std::max(2 * k, k + 256) + 31) / 32 * 32 : 0;  // >= k + one tile (128) of slack
   *pl = P;
@@ -711,6 +729,7 @@ int run_fused(fk_index* h, const Plan& P, int64_t nq, int64_t nb_pass, int k, bo
   sp.num_units = P.num_units;
   sp.num_kb = dpk / (h16 ? 64 : 32);
   sp.a_mode = P.a_mode;
+  sp.a_kt = P.a_kt;
   sp.stages = P.stages;
   sp.xn_slots = P.xn_slots;
   sp.acc_stages = P.acc_stages;

@@ -84,7 +84,8 @@ struct SearchParams {
   int num_m, n_tiles, chunk_tiles, S, num_units;
   int probe_tiles;  // > 0: chunk 0 is a short probe chunk [0, probe_tiles), the others follow it
   int num_kb;      // padded d / elements-per-128B-chunk
-  int a_mode;      // 0: queries in TMEM, 1: resident in smem, 2: streamed per stage
+  int a_mode;      // 0: queries in TMEM, 1: resident in smem, 2: streamed per stage, 3: split (below)
+  int a_kt;        // a_mode 3: K-chunks [0, a_kt) of the queries in TMEM, the rest resident in smem
   int stages;      // B (and streamed A) pipeline depth
   int xn_slots;    // base-norm tile ring depth (prefetched by the producer)
   unsigned long long* trace;  // debug timeline (CTA 0): [tile][16] clock64 stamps
@@ -316,6 +317,10 @@ __device__ __forceinline__ int warp_compact_le(uint64_t* buf, int cnt, uint64_t 
 // a_mode 0: queries in TMEM (TS MMA; frees smem, halves smem operand reads)
 // a_mode 1: queries resident in smem for the unit
 // a_mode 2: queries streamed with every B stage (large d)
+// a_mode 3: split -- the first a_kt K-chunks in TMEM (TS MMAs), the rest in
+//           smem (SS MMAs): a query operand too large for TMEM beside two
+//           accumulators (d = 768 16-bit) keeps two accumulators (no drain of
+//           the MMA pipe at every tile)
 constexpr int MAX_ACC = 4;      // TMEM accumulator buffers
 constexpr int MAX_STAGES = 32;  // smem operand ring  // TMEM accumulator buffers (runtime p.acc_stages); A operand columns follow them
 
@@ -388,7 +393,8 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
   const int num_kb = p.num_kb;
   const int stages = p.stages;
   const int a_mode = p.a_mode;
-  const uint32_t a_bytes = (a_mode == 1) ? SPLIT * num_kb * CHUNK_BYTES : 0u;
+  const int a_kt = (a_mode == 3) ? p.a_kt : (a_mode == 0 ? num_kb : 0);  // K-chunks of A in TMEM
+  const uint32_t a_bytes = (a_mode == 1 || a_mode == 3) ? SPLIT * (num_kb - a_kt) * CHUNK_BYTES : 0u;
   // stage = [B hi (| B lo)] (a_mode 2: + [A hi (| A lo)], 128-row chunks)
   const uint32_t stage_bytes = SPLIT * B_CHUNK + (a_mode == 2 ? SPLIT * CHUNK_BYTES : 0u);
   constexpr uint32_t tmem_cols = 512u;  // 1 CTA per SM: take the whole TMEM
@@ -440,7 +446,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       mbar_init(&xfull[x], 1);
       mbar_init(&xempty[x], 4);
     }
-    mbar_init(afull, a_mode == 0 ? EPI : 1);
+    mbar_init(afull, a_mode == 0 ? EPI : (a_mode == 3 ? EPI + 1 : 1));
     mbar_init(aempty, p.n_issuers);
     fence_mbar_init();
   }
@@ -475,12 +481,13 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         const int m = (u - chunk * p.num_mu) * CL + (int)crank;
         int t0, t1;
         chunk_range(p, chunk, t0, t1);
-        if (a_mode == 1 && myring == 0) {
+        if ((a_mode == 1 || a_mode == 3) && myring == 0) {  // smem-resident K-chunks [a_kt, num_kb)
           if (j > 0) mbar_wait(aempty, (j - 1) & 1);
           mbar_arrive_expect_tx(afull, a_bytes);
+          const int nka = num_kb - a_kt;
           for (int part = 0; part < SPLIT; ++part)
-            for (int kb = 0; kb < num_kb; ++kb)
-              tma_load_2d(a_region + (part * num_kb + kb) * CHUNK_BYTES, part ? &tm_a1 : &tm_a0, afull,
+            for (int kb = a_kt; kb < num_kb; ++kb)
+              tma_load_2d(a_region + (part * nka + kb - a_kt) * CHUNK_BYTES, part ? &tm_a1 : &tm_a0, afull,
                           kb * BK, m * BM, pol_a);
         }
         for (int t = t0; t < t1; ++t, ++tc) {
@@ -585,7 +592,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             const uint64_t bd0 = st_desc0 + ((stage * stage_bytes) >> 4);
             const uint64_t bd1 = bd0 + (B_CHUNK >> 4);
             if (elect_one()) {
-              if (a_mode == 0) {
+              if (a_mode == 0 || (a_mode == 3 && kb < a_kt)) {
                 const uint32_t ah = a_tm + kb * 32;
                 if (MODE == 0) {
 #pragma unroll
@@ -618,8 +625,8 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
                   }
                 }
               } else {
-                const uint64_t ad0 =
-                    (a_mode == 1) ? a_desc0 + ((kb * CHUNK_BYTES) >> 4) : bd0 + ((SPLIT * B_CHUNK) >> 4);
+                const uint64_t ad0 = (a_mode == 1 || a_mode == 3) ? a_desc0 + (((kb - a_kt) * CHUNK_BYTES) >> 4)
+                                                                  : bd0 + ((SPLIT * B_CHUNK) >> 4);
                 if (MODE == 0) {
                   const uint64_t ad1 = (a_mode == 1) ? a_desc0 + (((num_kb + kb) * CHUNK_BYTES) >> 4)
                                                      : bd0 + ((2 * B_CHUNK + CHUNK_BYTES) >> 4);
@@ -692,13 +699,14 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       const int row = m * BM + eq * 32 + lane;
       const bool row_ok = row < p.nq;
 
-      if (a_mode == 0) {
+      if (a_mode == 0 || a_mode == 3) {
         // Query tile -> TMEM (lane = query row, columns = K; fp32: [hi | lo]).
         // Only after EVERY MMA of the previous unit retired (both issuers
         // commit aempty at unit end): with two epilogue groups, this group's
         // last tile is not necessarily the unit's last MMA.
         if (uj > 0) mbar_wait(aempty, (uj - 1) & 1);
-        for (int cc = h; cc < a_cols / 32; cc += NH) {
+        const int a_ccn = (a_mode == 3) ? a_kt : a_cols / 32;  // 32-column groups written (a_mode 3: TMEM part)
+        for (int cc = h; cc < a_ccn; cc += NH) {
           uint32_t v[32];
           const uint32_t* src;
           if (MODE == 0)

@@ -415,26 +415,52 @@ def test_large_k_estimate_fails_certification_and_reruns():
     assert_parity(res.ids, res.distances, want_ids, want_dist)
 
 
+@pytest.mark.parametrize("storage,metric,nq", [("bf16", "l2", 300), ("fp16", "l2", 130), ("bf16", "ip", 257)])
+def test_split_query_operand_l2_and_ragged_tiles(storage, metric, nq):
+    """a_mode 3 on the L2 (base-norm tile) and bf16 paths, with a ragged last
+    query tile; equal to the whole-in-TMEM plan and to the oracle."""
+    rng = np.random.default_rng(769)
+    xb = rng.standard_normal((20000, 768), dtype=np.float32)
+    q = rng.standard_normal((nq, 768), dtype=np.float32)
+    idx = FlatIndex(768, METRIC_IP if metric == "ip" else METRIC_L2, storage=storage)
+    idx.add(xb)
+    base = idx.search(q, 10)
+    assert idx.last_plan()["a_mode"] == 3
+    os.environ["FK_AMODE3"] = "0"
+    try:
+        alt = idx.search(q, 10)
+        assert idx.last_plan()["a_mode"] == 0
+    finally:
+        del os.environ["FK_AMODE3"]
+    assert np.array_equal(base.ids, alt.ids) and np.array_equal(base.distances, alt.distances)
+    xr, qr = O.round_to(xb, storage), O.round_to(q, storage)
+    want_ids, want_dist = O.flat_search_blas(xr, qr, 10, metric)
+    assert_parity(base.ids, base.distances, want_ids, want_dist)
+
+
 @pytest.mark.parametrize("k", [10, 100])
 def test_large_query_operand_tile_plans(k):
-    """d = 768 16-bit (cfg4 shape): the query operand takes 384 TMEM columns;
-    the default plan keeps ONE 128-column accumulator next to it, FK_BN=64 the
-    round-1 plan of two 64-column accumulators -- identical answers, and the
-    oracle's on the rounded inputs."""
+    """d = 768 16-bit (cfg4 shape): the query operand needs 384 TMEM columns.
+    The default plan splits it (a_mode 3: 8 K-chunks in TMEM beside two
+    128-column accumulators, 4 in smem); FK_AMODE3=0 keeps it whole beside ONE
+    accumulator, FK_BN=64 the round-1 plan of two 64-column accumulators --
+    identical answers, and the oracle's on the rounded inputs."""
     rng = np.random.default_rng(768)
     xb = rng.standard_normal((30000, 768), dtype=np.float32)
     q = rng.standard_normal((200, 768), dtype=np.float32)
     idx = FlatIndex(768, METRIC_IP, storage="fp16")
     idx.add(xb)
     base = idx.search(q, k)
-    assert idx.last_plan()["bn"] == 128 and idx.last_plan()["acc_stages"] == 1
-    os.environ["FK_BN"] = "64"
-    try:
-        alt = idx.search(q, k)
-        assert idx.last_plan()["bn"] == 64
-    finally:
-        del os.environ["FK_BN"]
-    assert np.array_equal(base.ids, alt.ids) and np.array_equal(base.distances, alt.distances)
+    assert idx.last_plan()["bn"] == 128 and idx.last_plan()["a_mode"] == 3 and idx.last_plan()["acc_stages"] == 2
+    for env, check in (("FK_AMODE3", lambda p: p["a_mode"] == 0 and p["acc_stages"] == 1),
+                       ("FK_BN", lambda p: p["bn"] == 64)):
+        os.environ[env] = "0" if env == "FK_AMODE3" else "64"
+        try:
+            alt = idx.search(q, k)
+            assert check(idx.last_plan()), idx.last_plan()
+        finally:
+            del os.environ[env]
+        assert np.array_equal(base.ids, alt.ids) and np.array_equal(base.distances, alt.distances)
     xr, qr = O.round_to(xb, "fp16"), O.round_to(q, "fp16")
     want_ids, want_dist = O.flat_search_blas(xr, qr, k, "ip")
     assert_parity(base.ids, base.distances, want_ids, want_dist)

@@ -48,16 +48,18 @@ def test_gpu_range_matches_reference(name):
 @pytest.mark.gpu
 @pytest.mark.parametrize("storage", ["fp16", "bf16"])
 @pytest.mark.parametrize("metric", ["l2", "ip"])
-def test_gpu_range_16bit_storage_vs_oracle_on_rounded_inputs(storage, metric):
+@pytest.mark.parametrize("d", [96, 768])
+def test_gpu_range_16bit_storage_vs_oracle_on_rounded_inputs(storage, metric, d):
+    """(d = 768: the query operand is split between TMEM and smem, a_mode 3)"""
     import torch
     from paper_2401_08281_b200 import METRIC_IP, METRIC_L2, FlatIndex
     rng = np.random.default_rng(77)
-    xb = rng.standard_normal((20000, 96), dtype=np.float32)
-    q = rng.standard_normal((64, 96), dtype=np.float32)
+    xb = rng.standard_normal((20000 if d == 96 else 6000, d), dtype=np.float32)
+    q = rng.standard_normal((64, d), dtype=np.float32)
     xr, qr = O.round_to(xb, storage), O.round_to(q, storage)
     dm = O.direct_distances(qr[:8], xr, metric)
     radius = float(np.quantile(dm, 0.995 if metric == "ip" else 0.005))
-    idx = FlatIndex(96, METRIC_IP if metric == "ip" else METRIC_L2, storage=storage)
+    idx = FlatIndex(d, METRIC_IP if metric == "ip" else METRIC_L2, storage=storage)
     idx.add(xb)
     res = idx.range_search(torch.from_numpy(q).cuda(), radius)  # device in -> device out
     assert res.ids.is_cuda
