@@ -279,3 +279,26 @@ def test_filter16_mid_k_default_path(metric, k):
     finally:
         del os.environ["FK_FP32_3X"]
     assert_parity(res.ids, res.distances, r3.ids, r3.distances)
+
+
+@pytest.mark.parametrize("metric", ["l2", "ip"])
+def test_filter16_split_query_operand_d768(metric):
+    """d = 768 fp32: the scaled-fp16 query operand needs 384 TMEM columns, so
+    the 1-pass filter runs the split plan (a_mode 3) -- identical to the
+    whole-in-TMEM plan, and the oracle's answers."""
+    rng = np.random.default_rng(768)
+    xb = rng.standard_normal((20000, 768), dtype=np.float32)
+    q = rng.standard_normal((150, 768), dtype=np.float32)
+    idx = _index(768, metric)
+    idx.add(xb)
+    r = _search(idx, q, 10)
+    assert idx.last_plan()["kmode"] == 5 and idx.last_plan()["a_mode"] == 3
+    os.environ["FK_AMODE3"] = "0"
+    try:
+        r0 = _search(idx, q, 10)
+        assert idx.last_plan()["a_mode"] == 0
+    finally:
+        del os.environ["FK_AMODE3"]
+    assert np.array_equal(r.ids, r0.ids) and np.array_equal(r.distances, r0.distances)
+    want_ids, want_dist = O.flat_search_blas(xb, q, 10, metric)
+    assert_parity(r.ids, r.distances, want_ids, want_dist)
