@@ -221,7 +221,11 @@ struct fk_index {
 struct fk_range_result {
   int device = 0;
   int64_t total = 0;
-  DevBuf ids, dist;
+  // stream-ordered allocations from the device's default memory pool (a
+  // per-call cudaMalloc/cudaFree pair costs more than the search's kernels)
+  void* ids = nullptr;
+  void* dist = nullptr;
+  cudaStream_t stream = nullptr;
 };
 
 namespace {
@@ -405,6 +409,13 @@ int fk_create(int device, int d, int metric, int storage, fk_index** out) {
   }
   if (const char* e = getenv("FK_NO_FOLD"); e && atoi(e)) h->fold = 0;
   h->num_sms = prop.multiProcessorCount;
+  {  // range results come from the default pool: keep freed blocks cached
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   // {base, queries} exactness flags of the tf32 split (MODE 0/4) and of the
   // scaled fp16 filter operands (MODE 5)
   if (cudaMalloc((void**)&h->inexact, 4 * sizeof(unsigned int)) != cudaSuccess ||
@@ -1286,9 +1297,11 @@ int fk_range_search(fk_index* h, const void* q, int64_t nq, int dtype, float rad
       gather_u64_kernel<<<g, 256, 0, st>>>(v1, krd, nsel, kid2);
       CKL();
       CK(cub::DeviceRadixSort::SortPairs(h->rtmp.p, tb2, kid2, krd2, v1, v2, nsel, 0, 32 + row_bits, st));
-      if ((rc = res->ids.ensure(nsel * 8)) || (rc = res->dist.ensure(nsel * 4))) return rc;
-      gather_range_kernel<<<g, 256, 0, st>>>(v2, kid, rd, nsel, static_cast<int64_t*>(res->ids.p),
-                                             static_cast<float*>(res->dist.p));
+      res->stream = st;
+      CK(cudaMallocAsync(&res->ids, (size_t)nsel * 8, st));
+      CK(cudaMallocAsync(&res->dist, (size_t)nsel * 4, st));
+      gather_range_kernel<<<g, 256, 0, st>>>(v2, kid, rd, nsel, static_cast<int64_t*>(res->ids),
+                                             static_cast<float*>(res->dist));
       CKL();
     }
     res->total = nsel;
@@ -1322,8 +1335,8 @@ int fk_range_fetch(fk_range_result* r, int64_t* ids, float* dist, int64_t capaci
   CK(cudaSetDevice(r->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-  CK(cudaMemcpyAsync(ids, r->ids.p, (size_t)r->total * sizeof(int64_t), kind, st));
-  CK(cudaMemcpyAsync(dist, r->dist.p, (size_t)r->total * sizeof(float), kind, st));
+  CK(cudaMemcpyAsync(ids, r->ids, (size_t)r->total * sizeof(int64_t), kind, st));
+  CK(cudaMemcpyAsync(dist, r->dist, (size_t)r->total * sizeof(float), kind, st));
   CK(cudaStreamSynchronize(st));
   return FK_OK;
 }
@@ -1333,8 +1346,10 @@ int64_t fk_range_total(const fk_range_result* r) { return r ? r->total : -1; }
 void fk_range_free(fk_range_result* r) {
   if (!r) return;
   cudaSetDevice(r->device);
-  r->ids.release();
-  r->dist.release();
+  // ordered after every use on the search's stream (fk_range_fetch copies on
+  // its own stream and synchronizes before returning)
+  if (r->ids) cudaFreeAsync(r->ids, r->stream);
+  if (r->dist) cudaFreeAsync(r->dist, r->stream);
   delete r;
 }
 
