@@ -462,6 +462,8 @@ int fk_reset(fk_index* h) {
   if (!h) return set_err(FK_E_INVALID, "NULL index");
   std::lock_guard<std::mutex> g(h->mu);
   CK(cudaSetDevice(h->device));
+  // a search still in flight on another stream reads the scalars reset below
+  if (h->scratch_used) CK(cudaEventSynchronize(h->scratch_ev));
   CK(cudaMemset(h->xn_max, 0, sizeof(float)));
   CK(cudaMemset(h->inexact, 0, 4 * sizeof(unsigned int)));
   if (h->f16st.p) CK(cudaMemset(h->f16st.p, 0, sizeof(F16State)));

@@ -18,6 +18,8 @@ k-means assignment step, both on the GPU flat search.
 
 from __future__ import annotations
 
+import threading
+
 import numpy as np
 import torch
 
@@ -29,6 +31,23 @@ from .flat import FlatIndex, _stream_of
 # to |x|^2 + max|c|^2 (~2^-21 of GEMM rounding + 2^-23 of centroid rounding,
 # with a wide safety factor)
 _MARGIN = 2.0 ** -16
+
+
+# One reusable shortlist index per (device, d, metric): k-means calls the
+# assignment every iteration, and creating + freeing an index per call costs
+# more than the search (allocation; cudaFree synchronizes the device).
+_SHORTLIST: dict = {}
+_SHORTLIST_LOCK = threading.Lock()
+
+
+def _shortlist_index(device: int, d: int, by_ip: bool):
+    key = (device, d, bool(by_ip))
+    with _SHORTLIST_LOCK:
+        ent = _SHORTLIST.get(key)
+        if ent is None:
+            ent = (FlatIndex(d, METRIC_IP if by_ip else METRIC_L2, storage="fp32", device=device), threading.Lock())
+            _SHORTLIST[key] = ent
+    return ent
 
 
 def coarse_quantizer(d: int, spherical: bool = False, storage: str = "fp32", device: int | None = None) -> FlatIndex:
@@ -71,9 +90,11 @@ def kmeans_assign(x, centroids, by_ip: bool = False, shortlist: int = 8, device:
     stream = _stream_of(dev.index)
     kc = min(shortlist, nc)
     if kc < nc:
-        idx = FlatIndex(d, METRIC_IP if by_ip else METRIC_L2, storage="fp32", device=dev.index)
-        idx.add(ct.float())
-        res = idx.search(xt, kc)
+        idx, lock = _shortlist_index(dev.index, d, by_ip)
+        with lock:  # reset + add + search of one caller at a time (stream-ordered on the device)
+            idx.reset()
+            idx.add(ct.float())
+            res = idx.search(xt, kc)
         cand = res.ids.contiguous()
         approx = res.distances.contiguous()
         unc = torch.empty(n, dtype=torch.int32, device=dev)
