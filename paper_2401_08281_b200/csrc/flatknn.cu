@@ -550,6 +550,15 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   P.epi = h16 ? 8 : 4;
   if (const char* e = getenv(kmode == 5 ? "FK_EPI5" : "FK_EPI"); e && kq >= 0) P.epi = atoi(e) == 8 ? 8 : 4;
   P.nh = P.epi / 4;
+  // Long 16-bit searches with a light epilogue (folded norms or IP): ONE
+  // epilogue group.  Under the board's power cap fewer busy warps buy clock:
+  // cfg5 (100M rows) 281 -> 252 ms, 16M rows 39.0 -> 36.5 ms; at 1M rows
+  // (not capped) two groups stay 7-10 % faster.  Threshold in nq * rows * dp.
+  if (h16 && kmode != 5 && kq > 0 && (h->fold || h->metric == FK_METRIC_IP) &&
+      (double)nq * (double)nb_pass * (double)dpk >= 4e12 && !getenv("FK_EPI")) {
+    P.epi = 4;
+    P.nh = 1;
+  }
   P.num_m = (int)((nq + BM - 1) / BM);
   const int split = kmode == 0 ? 2 : 1;
   const int num_kb = dpk / (h16 ? 64 : 32);

@@ -361,6 +361,30 @@ def test_large_k_plan_invariance(force):
     assert np.array_equal(base.ids, want_ids)
 
 
+@pytest.mark.parametrize("storage,metric,d", [("bf16", "l2", 96), ("fp16", "ip", 128), ("bf16", "ip", 96)])
+def test_16bit_epilogue_width_invariance(storage, metric, d):
+    """Long fold / IP searches run one epilogue group (query operand in TMEM,
+    two accumulators) instead of two (A in smem, four): the same answers."""
+    rng = np.random.default_rng(96)
+    xb = rng.standard_normal((60000, d), dtype=np.float32)
+    q = rng.standard_normal((700, d), dtype=np.float32)
+    idx = FlatIndex(d, METRIC_IP if metric == "ip" else METRIC_L2, storage=storage)
+    idx.add(xb)
+    base = idx.search(q, 10)
+    assert idx.last_plan()["epi"] == 8
+    for width in ("4", "8"):
+        os.environ["FK_EPI"] = width
+        try:
+            alt = idx.search(q, 10)
+            assert idx.last_plan()["epi"] == int(width)
+        finally:
+            del os.environ["FK_EPI"]
+        assert np.array_equal(base.ids, alt.ids) and np.array_equal(base.distances, alt.distances)
+    xr, qr = O.round_to(xb, storage), O.round_to(q, storage)
+    want_ids, want_dist = O.flat_search_blas(xr, qr, 10, metric)
+    assert_parity(base.ids, base.distances, want_ids, want_dist)
+
+
 def test_k_equals_ntotal_large():
     rng = np.random.default_rng(1)
     idx = IndexFlatL2(4)
