@@ -28,6 +28,12 @@
 // experiment switch (variant builds): 1 = unrolled 4-MMA issue for full
 // K-chunks (A/B on cfg2: MMA-only 2.09 vs 2.19 ms but the full kernel 3.68 vs
 // 3.44 ms -- off)
+#ifndef FK_LD_X64  // 64-column TMEM loads in the two-group epilogue (0: two 32-column loads)
+#define FK_LD_X64 1
+#endif
+#ifndef FK_LD_X128  // one 128-column TMEM load in the one-group epilogue (experiment)
+#define FK_LD_X128 0
+#endif
 #ifndef FK_ISSUER_FAST
 #define FK_ISSUER_FAST 0
 #endif
@@ -987,10 +993,16 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
           uint32_t racc[PIECE];
           if (tr && pc == 0) p.trace[(tcount - TOFF) * 16 + 2] = clock64();
           if (do_epi) {
+            if constexpr (FK_LD_X64 && PIECE == 64) {  // one 64-column load
+              tmem_ld_32x32b_x64(tmem_base + lane_addr + buf * BN + pc * PIECE, racc);
+            } else if constexpr (FK_LD_X128 && PIECE == 128) {  // the whole tile row in one load
+              tmem_ld_32x32b_x128(tmem_base + lane_addr + buf * BN, racc);
+            } else {
 #pragma unroll
-            for (int c = 0; c < PIECE / 32; ++c)
-              tmem_ld_32x32b_x32(tmem_base + lane_addr + buf * BN + pc * PIECE + c * 32,
-                                 *reinterpret_cast<uint32_t(*)[32]>(&racc[32 * c]));
+              for (int c = 0; c < PIECE / 32; ++c)
+                tmem_ld_32x32b_x32(tmem_base + lane_addr + buf * BN + pc * PIECE + c * 32,
+                                   *reinterpret_cast<uint32_t(*)[32]>(&racc[32 * c]));
+            }
             tmem_ld_wait();
           }
           if (tr && pc < 2) p.trace[(tcount - TOFF) * 16 + 11 + pc] = clock64();
