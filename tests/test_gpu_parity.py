@@ -488,3 +488,27 @@ def test_large_query_operand_tile_plans(k):
     xr, qr = O.round_to(xb, "fp16"), O.round_to(q, "fp16")
     want_ids, want_dist = O.flat_search_blas(xr, qr, k, "ip")
     assert_parity(base.ids, base.distances, want_ids, want_dist)
+
+
+@pytest.mark.parametrize("d,storage,metric,k", [(520, "fp16", "l2", 1), (600, "bf16", "ip", 64), (700, "fp16", "ip", 100),
+                                                 (765, "bf16", "l2", 10), (768, "bf16", "l2", 33)])
+def test_split_query_operand_shapes(d, storage, metric, k):
+    """a_mode 3 across d in (512, 768] (d = 765 bf16 L2 folds its norms into
+    the last, smem-resident K-chunk), queue and candidate-buffer k: equal to
+    the whole-in-TMEM plan and to the oracle."""
+    rng = np.random.default_rng(d + k)
+    xb = rng.standard_normal((12000, d), dtype=np.float32)
+    q = rng.standard_normal((181, d), dtype=np.float32)
+    idx = FlatIndex(d, METRIC_IP if metric == "ip" else METRIC_L2, storage=storage)
+    idx.add(xb)
+    base = idx.search(q, k)
+    assert idx.last_plan()["a_mode"] == 3
+    os.environ["FK_AMODE3"] = "0"
+    try:
+        alt = idx.search(q, k)
+    finally:
+        del os.environ["FK_AMODE3"]
+    assert np.array_equal(base.ids, alt.ids) and np.array_equal(base.distances, alt.distances)
+    xr, qr = O.round_to(xb, storage), O.round_to(q, storage)
+    want_ids, want_dist = O.flat_search_blas(xr, qr, k, metric)
+    assert_parity(base.ids, base.distances, want_ids, want_dist)
