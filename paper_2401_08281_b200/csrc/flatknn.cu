@@ -91,6 +91,7 @@ constexpr int FK_MAX_K = 2048;
 constexpr int64_t FP32_1X_MIN_ROWS = 262144;
 constexpr size_t L2_CHUNK_BYTES = 48ull << 20;  // streamed base per N-chunk (2 chunks in flight << 126 MB L2)
 constexpr size_t PARTIAL_BYTES = 4ull << 30;    // split-N partial top-k lists
+constexpr int DIRECT_CHUNK = 8192;   // direct path: rows per first-level selection slice
 constexpr int MERGE_SMC = 16384;    // large-k merge: survivors gathered in smem (128 KB) + 2048 winners
 constexpr int SMEM_RESERVE = 1024 /*align*/ + 512 /*barriers + tmem slot*/;
 
@@ -630,7 +631,10 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   const int max_chunk = std::max<int>(16, (int)(l2_chunk * (k >= 512 ? 4 : 1) / tile_bytes));
   const int min_S = (P.n_tiles + max_chunk - 1) / max_chunk;
   const size_t list_bytes = (size_t)nq * P.nh * std::max(k, 1) * 8;  // one chunk's partial lists
-  const int max_S = (int)std::max<size_t>(1, std::min<size_t>(PARTIAL_BYTES / list_bytes, 1 << 20));
+  int max_S = (int)std::max<size_t>(1, std::min<size_t>(PARTIAL_BYTES / list_bytes, 1 << 20));
+  // 1-pass lists: every query's S x NH lists (+ its overflow list) must fit the
+  // rescoring merge's survivor buffer, else the query falls back to a scan
+  if ((kmode == 4 || kmode == 5) && kq > 0) max_S = std::max(1, std::min(max_S, (MERGE_SMC - 64) / (P.nh * std::max(k, 1))));
   plan_split(P.num_mu, P.n_tiles, h->num_sms / P.cluster, min_S, max_S, &P.S, &P.chunk_tiles);
   int fs = force_S;
   if (const char* e = getenv("FK_FORCE_S"); e && !force_S) fs = atoi(e);
@@ -816,6 +820,8 @@ int launch_merge(fk_index* h, const Plan& P, int64_t nq, int k, bool ip, float* 
     // 4k entries and 256 threads stay best, cfg4 k=100)
     const bool big_k = k >= 512;
     int smc = std::min(MERGE_SMC, std::max(1024, (big_k ? 8 : 4) * k));
+    if (nq <= 4 * (int64_t)h->num_sms)  // small batch: every list entry fits (no global-memory select)
+      smc = std::min(MERGE_SMC, std::max<int>(smc, P.S_tot * k));
     if (const char* e = getenv("FK_MERGE_SMC")) smc = std::max(1, std::min(MERGE_SMC, atoi(e)));
     int p2 = 1;
     while (p2 < k) p2 <<= 1;
@@ -1027,7 +1033,13 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
   int* fcount = static_cast<int*>(h->rfail.p) + 2 * nq;  // device list of uncertified queries
   int* flist = static_cast<int*>(h->rfail.p) + nq;
   CK(cudaMemsetAsync(fcount, 0, sizeof(int), st));
-  const int smc = std::min(MERGE_SMC, std::max(1024, 24 * kp));
+  // survivor buffer: 24 k' by default; a small batch (one query tile split
+  // over every SM: S_tot k' entries per query) gets room for all of its list
+  // and overflow entries -- few CTAs, and an overflow would send the query to
+  // the exact fallback (a scan of the whole base per query)
+  int smc = std::min(MERGE_SMC, std::max(1024, 24 * kp));
+  if (nq <= 4 * (int64_t)h->num_sms)
+    smc = std::min(MERGE_SMC, std::max<int>(smc, pl.S_tot * kp + ovf_cap));
   int p2 = 1;
   while (p2 < k) p2 <<= 1;
   static std::atomic<uint64_t> cfg{0};
@@ -1161,10 +1173,23 @@ int search_direct(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* d
       direct_dist_kernel<2><<<grid, 256, 0, st>>>(qa, nullptr, gq, h->s0, nullptr, n, h->d, h->dp, ip, h->fold, comp);
     CKL();
     if (ev && g0 == 0) CK(cudaEventRecord(ev[2], st));
+    // two-level selection when the rows outnumber the slices' k-lists
+    const uint64_t* sel_in = comp;
+    int64_t sel_n = n;
+    const int64_t nch = (n + DIRECT_CHUNK - 1) / DIRECT_CHUNK;
+    if (nch > 1 && nch * k < n) {
+      if ((rc = h->rkid.ensure((size_t)gq * nch * k * 8))) return rc;
+      auto part = static_cast<uint64_t*>(h->rkid.p);
+      direct_chunk_topk_kernel<<<dim3((unsigned)nch, (unsigned)gq), 256, 0, st>>>(comp, n, DIRECT_CHUNK, k, part);
+      CKL();
+      h->nlaunch++;
+      sel_in = part;
+      sel_n = nch * k;
+    }
     if (ip)
-      direct_select_kernel<true><<<gq, 256, (size_t)p2 * 8, st>>>(comp, n, (int)g0, k, h->ids, dD, dI, dP);
+      direct_select_kernel<true><<<gq, 256, (size_t)p2 * 8, st>>>(sel_in, sel_n, (int)g0, k, h->ids, dD, dI, dP);
     else
-      direct_select_kernel<false><<<gq, 256, (size_t)p2 * 8, st>>>(comp, n, (int)g0, k, h->ids, dD, dI, dP);
+      direct_select_kernel<false><<<gq, 256, (size_t)p2 * 8, st>>>(sel_in, sel_n, (int)g0, k, h->ids, dD, dI, dP);
     CKL();
     h->nlaunch += 2;
   }

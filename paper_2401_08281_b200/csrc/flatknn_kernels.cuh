@@ -443,8 +443,8 @@ __global__ void __launch_bounds__(256) merge_rescore_kernel(
   // accumulation slack (4 dp + 8) 2^-23 (qn + max xn) (same as the fused
   // kernel's band4)
   const bool tf32_exact = inexact != nullptr && (inexact[0] | inexact[1]) == 0u;
-  const float e2 = (tf32_exact ? 0.f : (IS_IP ? 0.5f * band_l2 : band_l2)) * sqrtf(fmaxf(qn, 0.f) * fmaxf(*xn_max, 0.f)) +
-                   (4.f * (float)dp + 8.f) * 1.1920928955078125e-07f * (fmaxf(qn, 0.f) + fmaxf(*xn_max, 0.f));
+  const float e2 = (tf32_exact ? 0.f : (IS_IP ? 0.5f * band_l2 : band_l2)) * sqrtf(band_norm(qn) * band_norm(*xn_max)) +
+                   (4.f * (float)dp + 8.f) * 1.1920928955078125e-07f * (band_norm(qn) + band_norm(*xn_max));
   bool ok = true;
   int why = 0;
   uint32_t band_key = 0xFFFFFFFFu;  // only entries with t <= t_k + band can be in the exact top-k
@@ -634,8 +634,8 @@ __global__ void __launch_bounds__(256) merge_rescore_warp_kernel(
   };
   const float qn = qnorm[q];
   const bool tf32_exact = inexact != nullptr && (inexact[0] | inexact[1]) == 0u;
-  const float e2 = (tf32_exact ? 0.f : (IS_IP ? 0.5f * band_l2 : band_l2)) * sqrtf(fmaxf(qn, 0.f) * fmaxf(*xn_max, 0.f)) +
-                   (4.f * (float)dp + 8.f) * 1.1920928955078125e-07f * (fmaxf(qn, 0.f) + fmaxf(*xn_max, 0.f));
+  const float e2 = (tf32_exact ? 0.f : (IS_IP ? 0.5f * band_l2 : band_l2)) * sqrtf(band_norm(qn) * band_norm(*xn_max)) +
+                   (4.f * (float)dp + 8.f) * 1.1920928955078125e-07f * (band_norm(qn) + band_norm(*xn_max));
   uint32_t band_key = 0xFFFFFFFFu;
   int why = 0;
   if (n >= k) {
@@ -858,6 +858,31 @@ __global__ void __launch_bounds__(256) direct_dist_kernel(const void* __restrict
       comp[(size_t)qi * n + r] = (static_cast<uint64_t>(dist_key(v, is_ip != 0)) << 32) | static_cast<uint32_t>(r);
     }
   }
+}
+
+// Direct path, first selection level: the exact k smallest composites of
+// each `chunk`-row slice of one query's row (grid: slices x queries), padded
+// with ~0 to k -- the per-query selection then runs over slices x k entries
+// instead of every row (one CTA over 1M composites took milliseconds).
+__global__ void __launch_bounds__(256) direct_chunk_topk_kernel(const uint64_t* __restrict__ comp, int64_t n,
+                                                                int chunk, int k, uint64_t* __restrict__ out) {
+  __shared__ uint32_t hist[256], sel[8];
+  __shared__ int cnt_out;
+  const int64_t c0 = (int64_t)blockIdx.x * chunk;
+  const int64_t left = n - c0;
+  const int cnt = left < (int64_t)chunk ? (int)left : chunk;
+  const uint64_t* src = comp + (size_t)blockIdx.y * n + c0;
+  uint64_t* dst = out + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * k;
+  if (threadIdx.x == 0) cnt_out = 0;
+  __syncthreads();
+  uint64_t kth = ~0ull;  // valid composites are < ~0 (keys < 0xFFFFFFFF)
+  if (cnt > k) kth = block_kth([&](int e) { return __ldg(src + e); }, cnt, (uint32_t)k, hist, sel);
+  for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+    const uint64_t v = __ldg(src + e);
+    if (v <= kth) dst[atomicAdd(&cnt_out, 1)] = v;
+  }
+  __syncthreads();
+  for (int i = cnt_out + threadIdx.x; i < k; i += blockDim.x) dst[i] = ~0ull;
 }
 
 template <bool IS_IP>

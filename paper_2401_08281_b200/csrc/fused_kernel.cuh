@@ -771,13 +771,13 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       // (+ 2^-10 margin)
       const float band4 = (F1P && KQ > 0 && !RANGE && row_ok)
                               ? (tf32_exact ? 0.f : (IS_IP ? 0.5f * p.band_l2 : p.band_l2)) *
-                                        sqrtf(fmaxf(p.qnorm[row], 0.f) * fmaxf(*p.xn_max, 0.f)) +
+                                        sqrtf(band_norm(p.qnorm[row]) * band_norm(*p.xn_max)) +
                                     // fp32 accumulation: the tensor core (possibly truncating,
                                     // <= dp 2^-23) and the sequential-FMA rescoring (<= dp 2^-24)
                                     // each err by <= dp u (qn + max xn); band = 2e, 2x safety,
                                     // + the final (qn + xn) - 2ip roundings
                                     (4.f * (float)dp + 8.f) * 1.1920928955078125e-07f *
-                                        (fmaxf(p.qnorm[row], 0.f) + fmaxf(*p.xn_max, 0.f))
+                                        (band_norm(p.qnorm[row]) + band_norm(*p.xn_max))
                               : 0.f;
       uint32_t min_lost = 0xFFFFFFFFu;  // F1P: smallest band key lost (overflow list full)
       // queue slot of the caller's k-th (MODE 4 keeps k' >= kfinal entries);

@@ -1,0 +1,3 @@
+#!/bin/bash
+timeout 600 python scripts/small_batch.py 2>&1 | tail -6
+timeout 1500 python -m pytest tests/test_direct_path.py tests/test_fp32_filter16.py tests/test_edge_values.py tests/test_gpu_parity.py -m gpu -q -x --timeout 900 2>&1 | tail -2

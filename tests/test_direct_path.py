@@ -87,3 +87,20 @@ def test_direct_device_tensors_and_ids():
     assert res.ids.is_cuda
     want_ids, want_dist = O.flat_search_direct(xb, q, 9, "ip", ids=ids)
     assert_parity(res.ids.cpu().numpy(), res.distances.cpu().numpy(), want_ids, want_dist)
+
+
+@pytest.mark.parametrize("metric", ["l2", "ip"])
+@pytest.mark.parametrize("nq,k,nb", [(1, 10, 100_000), (5, 1, 70_000), (19, 100, 50_001), (3, 2048, 40_000)])
+def test_direct_two_level_selection(metric, nq, k, nb):
+    """More rows than 8192-row slices x k: each slice's exact top-k first,
+    then the per-query selection over the slices' lists -- the oracle's
+    direct answers, ties by position."""
+    rng = np.random.default_rng(nb + k)
+    xb = rng.integers(-3, 4, size=(nb, 24)).astype(np.float32)  # many exact ties
+    q = rng.integers(-3, 4, size=(nq, 24)).astype(np.float32)
+    idx = FlatIndex(24, METRIC_L2 if metric == "l2" else METRIC_IP)
+    idx.add(xb)
+    res = idx.search(q, k)
+    assert idx.last_plan()["kmode"] == -1
+    want_ids, want_dist = O.flat_search_direct(xb, q, k, metric)
+    assert np.array_equal(res.ids, want_ids) and np.array_equal(res.distances, want_dist)

@@ -302,3 +302,25 @@ def test_filter16_split_query_operand_d768(metric):
     assert np.array_equal(r.ids, r0.ids) and np.array_equal(r.distances, r0.distances)
     want_ids, want_dist = O.flat_search_blas(xb, q, 10, metric)
     assert_parity(r.ids, r.distances, want_ids, want_dist)
+
+
+@pytest.mark.parametrize("nq", [20, 64, 129])
+@pytest.mark.parametrize("nan_rows", [False, True])
+def test_filter16_small_batches(nq, nan_rows):
+    """One query tile split over every SM: S x 2 lists of k' per query.  The
+    rescoring merge holds all of them (no spurious exact fallback -- a
+    whole-base scan per query), and NaN rows (a NaN max norm) widen the band
+    to infinity: those searches are answered exactly by the fallback."""
+    rng = np.random.default_rng(nq)
+    nb, d = 270_000, 32
+    xb = rng.standard_normal((nb, d), dtype=np.float32)
+    if nan_rows:
+        xb[[5, 77, nb - 1], 3] = np.nan
+    q = rng.standard_normal((nq, d), dtype=np.float32)
+    idx = _index(d, "l2")
+    idx.add(xb)
+    r = _search(idx, q, 10)
+    assert idx.last_plan()["kmode"] == 5
+    with np.errstate(invalid="ignore"):
+        want_ids, want_dist = O.flat_search_blas(xb, q, 10, "l2")
+    assert_parity(r.ids, r.distances, want_ids, want_dist)
