@@ -813,6 +813,85 @@ __device__ __forceinline__ double stored_val(const void* a, const void* b, size_
   return (double)__bfloat162float(static_cast<const __nv_bfloat16*>(a)[off]);
 }
 
+// Direct distances, a warp per stored row (d <= 256, the row in registers),
+// the staged queries in smem as doubles, 8 queries per reduction: a
+// transposing butterfly (xor 16 / 8 / 4 exchange halves of the 8 partial sums,
+// xor 2 / 1 finish) costs 9 double shuffles instead of 40 -- and adds the
+// same pairs in the same order as direct_dist_kernel, so the values are
+// bit-identical to it.
+template <int MODE>
+__global__ void __launch_bounds__(256) direct_dist_warp8_kernel(const void* __restrict__ q0,
+                                                                const void* __restrict__ q1, int nq,
+                                                                const void* __restrict__ s0,
+                                                                const void* __restrict__ s1, int64_t n, int d, int dp,
+                                                                int is_ip, int fold, uint64_t* __restrict__ comp) {
+  extern __shared__ double qs[];  // [nq][d]
+  for (int i = threadIdx.x; i < nq * d; i += blockDim.x) {
+    const int qi = i / d, c = i - qi * d;
+    qs[i] = stored_val<MODE>(q0, q1, (size_t)qi * dp + c);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  // grid-stride over rows: the query staging above is paid once per CTA
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n;
+       r += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+  constexpr int XR = 8;
+  double xv[XR];
+#pragma unroll
+  for (int i = 0; i < XR; ++i) {
+    const int c = lane + 32 * i;
+    xv[i] = c < d ? stored_val<MODE>(s0, s1, (size_t)r * dp + c) * (fold ? -0.5 : 1.0) : 0.0;  // -2x folded (exact)
+  }
+  for (int qb = 0; qb < nq; qb += 8) {
+    double v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      double acc = 0.0;
+      if (qb + j < nq) {
+        const double* qrow = qs + (size_t)(qb + j) * d;
+#pragma unroll
+        for (int i = 0; i < XR; ++i) {
+          const int c = lane + 32 * i;
+          if (c < d) {
+            const double qv = qrow[c];
+            if (is_ip) acc = fma(qv, xv[i], acc);
+            else {
+              const double t = qv - xv[i];
+              acc = fma(t, t, acc);
+            }
+          }
+        }
+      }
+      v[j] = acc;
+    }
+    // xor 16: lanes without bit 4 keep sums 0-3, lanes with it 4-7
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool hi = lane & 16;
+      const double send = hi ? v[j] : v[j + 4], keep = hi ? v[j + 4] : v[j];
+      v[j] = keep + __shfl_xor_sync(FULLMASK, send, 16);
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {  // xor 8
+      const bool hi = lane & 8;
+      const double send = hi ? v[j] : v[j + 2], keep = hi ? v[j + 2] : v[j];
+      v[j] = keep + __shfl_xor_sync(FULLMASK, send, 8);
+    }
+    {  // xor 4
+      const bool hi = lane & 4;
+      const double send = hi ? v[0] : v[1], keep = hi ? v[1] : v[0];
+      v[0] = keep + __shfl_xor_sync(FULLMASK, send, 4);
+    }
+    v[0] += __shfl_xor_sync(FULLMASK, v[0], 2);
+    v[0] += __shfl_xor_sync(FULLMASK, v[0], 1);
+    const int qi = qb + ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+    if ((lane & 3) == 0 && qi < nq)
+      comp[(size_t)qi * n + r] =
+          (static_cast<uint64_t>(dist_key(static_cast<float>(v[0]), is_ip != 0)) << 32) | static_cast<uint32_t>(r);
+  }
+  }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(256) direct_dist_kernel(const void* __restrict__ q0, const void* __restrict__ q1,
                                                           int nq, const void* __restrict__ s0,

@@ -104,3 +104,23 @@ def test_direct_two_level_selection(metric, nq, k, nb):
     assert idx.last_plan()["kmode"] == -1
     want_ids, want_dist = O.flat_search_direct(xb, q, k, metric)
     assert np.array_equal(res.ids, want_ids) and np.array_equal(res.distances, want_dist)
+
+
+@pytest.mark.parametrize("storage,metric,nq,d", [("fp32", "l2", 19, 128), ("fp16", "ip", 9, 96), ("bf16", "l2", 5, 200),
+                                                  ("fp32", "ip", 2, 33)])
+def test_direct_batched_reduction_bit_identical(storage, metric, nq, d):
+    """The 8-query transposing reduction adds the same pairs in the same
+    order as the one-query-at-a-time butterfly: bit-identical distances."""
+    import os
+    rng = np.random.default_rng(nq * d)
+    xb = rng.standard_normal((20000, d), dtype=np.float32)
+    q = rng.standard_normal((nq, d), dtype=np.float32)
+    idx = FlatIndex(d, METRIC_L2 if metric == "l2" else METRIC_IP, storage=storage)
+    idx.add(xb)
+    a = idx.search(q, 25)
+    os.environ["FK_DIRECT_WARP1"] = "1"
+    try:
+        b = idx.search(q, 25)
+    finally:
+        del os.environ["FK_DIRECT_WARP1"]
+    assert np.array_equal(a.ids, b.ids) and np.array_equal(a.distances, b.distances)
