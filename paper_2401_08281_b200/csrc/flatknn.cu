@@ -1511,6 +1511,9 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
     int64_t m_est = 0;
     if (kq == 0 && !getenv("FK_NO_EST")) {
       m_est = ((h->ntotal * 8) / k + BN - 1) / BN * BN;
+      // at least 32 tiles, while that sample still estimates a rank >= 2k
+      // (256 <= rows/k < 512; 300k rows, k = 1000, 100 queries: 6.2 -> 0.74 ms)
+      if (m_est < 32 * BN && (int64_t)32 * BN * k <= h->ntotal * 16) m_est = 32 * BN;
       if (m_est < 32 * BN || m_est * 8 > h->ntotal) m_est = 0;
     }
     if ((rc = h->thr.ensure((size_t)nq * sizeof(uint32_t)))) return rc;

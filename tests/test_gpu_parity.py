@@ -512,3 +512,18 @@ def test_split_query_operand_shapes(d, storage, metric, k):
     xr, qr = O.round_to(xb, storage), O.round_to(q, storage)
     want_ids, want_dist = O.flat_search_blas(xr, qr, k, metric)
     assert_parity(base.ids, base.distances, want_ids, want_dist)
+
+
+@pytest.mark.parametrize("storage,metric", [("fp16", "l2"), ("fp32", "ip")])
+def test_large_k_estimate_small_ratio(storage, metric):
+    """rows/k between 256 and 512 (300k rows, k = 1000): the estimated
+    large-k bound samples 32 tiles; certified or rerun, the oracle's answers."""
+    rng = np.random.default_rng(1000)
+    xb = rng.standard_normal((300_000, 32), dtype=np.float32)
+    q = rng.standard_normal((40, 32), dtype=np.float32)
+    idx = FlatIndex(32, METRIC_IP if metric == "ip" else METRIC_L2, storage=storage)
+    idx.add(xb)
+    res = idx.search(q, 1000)
+    xr, qr = O.round_to(xb, storage), O.round_to(q, storage)
+    want_ids, want_dist = O.flat_search_blas(xr, qr, 1000, metric)
+    assert_parity(res.ids, res.distances, want_ids, want_dist)
