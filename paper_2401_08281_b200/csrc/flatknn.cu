@@ -1514,6 +1514,10 @@ int fk_search(fk_index* h, const void* q, int64_t nq, int dtype, int k, float* D
       // at least 32 tiles, while that sample still estimates a rank >= 2k
       // (256 <= rows/k < 512; 300k rows, k = 1000, 100 queries: 6.2 -> 0.74 ms)
       if (m_est < 32 * BN && (int64_t)32 * BN * k <= h->ntotal * 16) m_est = 32 * BN;
+      // small k (33..~63): 8 rows/k would exceed an eighth of the rows; an
+      // eighth (at most 256 tiles) still estimates a rank >= 256 >= 2k
+      if (m_est * 8 > h->ntotal && k <= 128 && !getenv("FK_EST_SMALLK0"))
+        m_est = std::min<int64_t>(h->ntotal / 8, 256 * BN) / BN * BN;
       if (m_est < 32 * BN || m_est * 8 > h->ntotal) m_est = 0;
     }
     if ((rc = h->thr.ensure((size_t)nq * sizeof(uint32_t)))) return rc;
