@@ -72,6 +72,10 @@ class FlatIndex(Index):
     mode and the CUDA device ordinal.
     """
 
+    # exhaustive index: annkit's IVF search charges nlist coarse distances per
+    # query for a flat coarse quantizer (ivf.py:401; INTEGRATION.md §3b)
+    is_flat = True
+
     def __init__(self, d: int, metric: Metric = METRIC_L2, storage: str = "fp32", device: int | None = None):
         super().__init__(d, metric)
         mv = metric_value(metric)

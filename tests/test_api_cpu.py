@@ -124,3 +124,11 @@ def test_flat_index_rejects_unsupported_metric_before_touching_gpu():
         FlatIndex(0)
     with pytest.raises(ValueError):
         FlatIndex(4, storage="int8")
+
+
+def test_flat_index_marks_itself_flat_for_ivf_coarse_cost():
+    # annkit's IVF search charges nlist coarse distances per query only for a
+    # flat coarse quantizer (ivf.py:401); the GPU index answers the duck-typed
+    # check of the INTEGRATION.md patch (class attribute: no GPU needed)
+    from paper_2401_08281_b200.flat import FlatIndex, IndexFlatIP, IndexFlatL2
+    assert FlatIndex.is_flat and IndexFlatL2.is_flat and IndexFlatIP.is_flat
