@@ -29,6 +29,11 @@ def raw(rep):
     return dict(zip(rows[0], rows[2])), dict(zip(rows[0], rows[1]))
 
 
+def to_ms(v, unit):
+    return float(v.replace(",", "")) * {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1, "msecond": 1,
+                                         "s": 1e3, "second": 1e3}.get(unit, 1)
+
+
 def to_bytes(v, unit):
     v = float(v.replace(",", ""))
     return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
@@ -36,7 +41,8 @@ def to_bytes(v, unit):
 
 traffic = {}
 for rep, name in ((f"full_{tag}.ncu-rep", "cfg2"), (f"full2_{tag}.ncu-rep", "cfg2"), (f"full3_{tag}.ncu-rep", "cfg3"),
-                  (f"full4_{tag}.ncu-rep", "cfg4_2M"), (f"full5_{tag}.ncu-rep", "cfg5_2M")):
+                  (f"full4_{tag}.ncu-rep", "cfg4_2M"), (f"full5_{tag}.ncu-rep", "cfg5_2M"),
+                  (f"full3b_{tag}.ncu-rep", "cfg3_boundpass"), (f"full5b_{tag}.ncu-rep", "cfg5_4M")):
     p = os.path.join(reps, rep)
     if not os.path.exists(p):
         continue
@@ -48,7 +54,7 @@ for rep, name in ((f"full_{tag}.ncu-rep", "cfg2"), (f"full2_{tag}.ncu-rep", "cfg
     rd = to_bytes(r["dram__bytes_read.sum"], u["dram__bytes_read.sum"])
     wr = to_bytes(r["dram__bytes_write.sum"], u["dram__bytes_write.sum"])
     traffic[name] = {"kernel": r["Kernel Name"], "dram_read_bytes": rd, "dram_write_bytes": wr,
-                     "traffic_bytes": rd + wr, "duration_ms": float(r["gpu__time_duration.sum"].replace(",", "")),
+                     "traffic_bytes": rd + wr, "duration_ms": to_ms(r["gpu__time_duration.sum"], u["gpu__time_duration.sum"]),
                      "capture": os.path.relpath(os.path.join(dst, f"ncu_full_fused_{name}.txt"), REPO)}
 print("summaries ->", dst)
 for c in range(1, 6):  # per-config bench lines of the evidence pass (last JSON line of each)
