@@ -549,6 +549,9 @@ int make_plan(fk_index* h, int64_t nq, int64_t nb_pass, int k, int kq, int force
   // 16-bit operands: 2 epilogue warps per TMEM lane quarter (the epilogue, not
   // the MMA, paces a 16-bit tile); fp32 3xTF32 is MMA-paced -> 1 per quarter
   P.epi = h16 ? 8 : 4;
+  // 32-deep queues of the fp32 filter (12 < k <= 16): one group per quarter
+  // (two spill: cfg2 shape, k = 16: 5.7 ms vs 8.4)
+  if (kmode == 5 && kq == 32) P.epi = 4;
   if (const char* e = getenv(kmode == 5 ? "FK_EPI5" : "FK_EPI"); e && kq >= 0) P.epi = atoi(e) == 8 ? 8 : 4;
   P.nh = P.epi / 4;
   // Long 16-bit searches with a light epilogue (folded norms or IP): ONE
@@ -971,8 +974,13 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
   if (kmode == 5 && (rc = ensure_f16_base(h, st))) return rc;
   // k' >= k entries per list, the slack absorbs the tf32 band around the k-th
   // (register queues of 16 with the per-query overflow lists: measured
-  // cfg2 3.7 ms fused vs 5.6 with 32-deep queues, 0 of 10k uncertified)
-  int kp = k <= 4 ? 8 : k <= 16 ? 16 : std::min(k + std::max(64, k / 4), FK_MAX_K);
+  // cfg2 3.7 ms fused vs 5.6 with 32-deep queues, 0 of 10k uncertified).
+  // The slack k' - k must stay >= 4: every entry a full queue drops within
+  // the band goes to the 64-entry overflow list, and with k' = k (k = 16) it
+  // overflows for every query -> the whole-base exact fallback (cfg2 shape,
+  // k = 16: 3277 ms; k = 14: 54 ms, 204 ms at 1k queries).  12 < k <= 16
+  // take 32-deep queues (5.7 ms at k = 16, 0 uncertified).
+  int kp = k <= 4 ? 8 : k <= 12 ? 16 : k <= 16 ? 32 : std::min(k + std::max(64, k / 4), FK_MAX_K);
   if (const char* e = getenv("FK_KP")) kp = std::max(k, std::min(atoi(e), FK_MAX_K));
   const int kq = kp <= 8 ? 8 : kp <= 16 ? 16 : kp <= 32 ? 32 : 0;
   Plan pl;

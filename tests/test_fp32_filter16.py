@@ -324,3 +324,36 @@ def test_filter16_small_batches(nq, nan_rows):
     with np.errstate(invalid="ignore"):
         want_ids, want_dist = O.flat_search_blas(xb, q, 10, "l2")
     assert_parity(r.ids, r.distances, want_ids, want_dist)
+
+
+@pytest.mark.parametrize("metric", ["l2", "ip"])
+@pytest.mark.parametrize("k", [12, 13, 14, 16])
+def test_filter16_queue_slack_up_to_k16(metric, k):
+    """Register queues keep k' - k >= 4 slots of slack (k <= 12: k' = 16;
+    12 < k <= 16: k' = 32).  With k' = k a full queue drops a band member at
+    almost every late insertion, the 64-entry overflow lists overflow and every
+    query went to the whole-base exact fallback (k = 16 on 1M rows, 10k
+    queries: 3.3 s instead of 5.7 ms).  Same answers as the oracle, and no
+    fallback-sized slowdown against k = 10 on the same index."""
+    import time
+    rng = np.random.default_rng(1600 + k)
+    nb, d, nq = 300_000, 32, 1000
+    xb = rng.standard_normal((nb, d), dtype=np.float32)
+    q = rng.standard_normal((nq, d), dtype=np.float32)
+    from paper_2401_08281_b200 import METRIC_IP, METRIC_L2, FlatIndex
+    idx = FlatIndex(d, METRIC_IP if metric == "ip" else METRIC_L2, storage="fp32")
+    idx.add(xb)
+
+    def timed(kk):
+        idx.search(q, kk)
+        t0 = time.perf_counter()
+        r = idx.search(q, kk)  # host arrays: returns after the device work
+        return r, time.perf_counter() - t0
+
+    _, t10 = timed(10)
+    res, tk = timed(k)
+    plan = idx.last_plan()
+    assert plan["kmode"] == 5 and plan["kq"] // 100 == (16 if k <= 12 else 32)
+    assert tk < 10 * t10 + 0.005, (tk, t10)
+    want_ids, want_dist = O.flat_search_blas(xb, q[:200], k, metric)
+    assert_parity(res.ids[:200], res.distances[:200], want_ids, want_dist)
