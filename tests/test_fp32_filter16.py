@@ -357,3 +357,23 @@ def test_filter16_queue_slack_up_to_k16(metric, k):
     assert tk < 10 * t10 + 0.005, (tk, t10)
     want_ids, want_dist = O.flat_search_blas(xb, q[:200], k, metric)
     assert_parity(res.ids[:200], res.distances[:200], want_ids, want_dist)
+
+
+@pytest.mark.parametrize("d,nb", [(256, 300_000), (768, 270_000)])
+@pytest.mark.parametrize("nq", [20, 2000])
+def test_filter16_k16_wide_rows(d, nb, nq):
+    """32-deep queues with one epilogue group beside the wide query operands
+    (d = 256: whole in TMEM; d = 768: the split plan), few and many query
+    tiles: the oracle's answers."""
+    rng = np.random.default_rng(d + nq)
+    xb = rng.standard_normal((nb, d), dtype=np.float32)
+    q = rng.standard_normal((nq, d), dtype=np.float32)
+    from paper_2401_08281_b200 import METRIC_L2, FlatIndex
+    idx = FlatIndex(d, METRIC_L2, storage="fp32")
+    idx.add(xb)
+    res = idx.search(q, 16)
+    plan = idx.last_plan()
+    assert plan["kmode"] == 5 and plan["kq"] // 100 == 32
+    sub = slice(0, 40)
+    want_ids, want_dist = O.flat_search_blas(xb, q[sub], 16, "l2")
+    assert_parity(res.ids[sub], res.distances[sub], want_ids, want_dist)
