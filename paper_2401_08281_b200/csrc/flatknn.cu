@@ -1139,6 +1139,22 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
     return rc;
   auto comp = static_cast<uint64_t*>(h->rcomp.p);
   const size_t ssm = (size_t)p2 * 8;
+  const unsigned dgrid = 2u * (unsigned)h->num_sms;
+  if (ip)
+    fallback_dist_kernel<true><<<dgrid, 256, 0, st>>>(fcount, flist, nslots, q0, q1, qn, xb, xl, h->norms, h->ntotal,
+                                                      h->dp, comp);
+  else
+    fallback_dist_kernel<false><<<dgrid, 256, 0, st>>>(fcount, flist, nslots, q0, q1, qn, xb, xl, h->norms,
+                                                       h->ntotal, h->dp, comp);
+  CKL();
+  if (ip)
+    fallback_select_kernel<true><<<nslots, 1024, ssm, st>>>(fcount, flist, nslots, h->ntotal, k, h->ids, dD, dI, dP,
+                                                            comp);
+  else
+    fallback_select_kernel<false><<<nslots, 1024, ssm, st>>>(fcount, flist, nslots, h->ntotal, k, h->ids, dD, dI, dP,
+                                                             comp);
+  CKL();
+  h->nlaunch += 2;
   if (ip)
     fallback_kernel<true><<<nslots, 256, ssm, st>>>(fcount, flist, q0, q1, qn, xb, xl, h->norms, h->ntotal, h->dp, k,
                                                     h->ids, dD, dI, dP, comp);

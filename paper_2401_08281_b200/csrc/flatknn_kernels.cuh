@@ -758,6 +758,60 @@ __device__ void block_select_write(const uint64_t* comp, int nn, int k, int q, u
   __syncthreads();
 }
 
+// Exact composites of the first `nslots` failed queries (slot f = failed
+// query f), their rows split over the whole grid: a few uncertified queries
+// no longer scan the base with one CTA each (1M rows: ~25 ms per query).
+// fallback_select_kernel selects for those slots; fallback_kernel takes the
+// failed queries past them (whole-base scan per CTA).
+template <bool IS_IP>
+__global__ void __launch_bounds__(256) fallback_dist_kernel(const int* __restrict__ fail_count,
+                                                            const int* __restrict__ fail_list, int nslots,
+                                                            const float* __restrict__ q0, const float* __restrict__ q1,
+                                                            const float* __restrict__ qnorm, const float* __restrict__ xb,
+                                                            const float* __restrict__ xl,
+                                                            const float* __restrict__ xnorm, int64_t n, int dp,
+                                                            uint64_t* __restrict__ scratch) {
+  const int nf = min(*fail_count, nslots);
+  if (nf == 0) return;
+  const int R = max(1, (int)gridDim.x / nf);  // row ranges per failed query
+  const int64_t span = (n + R - 1) / R;
+  for (int w = blockIdx.x; w < nf * R; w += gridDim.x) {
+    const int f = w / R;
+    const int64_t r0 = (int64_t)(w - f * R) * span, r1 = min(n, r0 + span);
+    const int q = fail_list[f];
+    const float qn = qnorm[q];
+    const float4* qh = reinterpret_cast<const float4*>(q0 + (size_t)q * dp);
+    const float4* ql = q1 ? reinterpret_cast<const float4*>(q1 + (size_t)q * dp) : nullptr;
+    uint64_t* comp = scratch + (size_t)f * n;
+    for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {  // the same values as fallback_kernel
+      const float acc = thread_exact_dot(qh, ql, reinterpret_cast<const float4*>(xb + (size_t)r * dp),
+                                         xl ? reinterpret_cast<const float4*>(xl + (size_t)r * dp) : nullptr, dp);
+      float v = acc;
+      if (!IS_IP) {
+        v = fmaf(-2.f, acc, qn + xnorm[r]);
+        v = (v <= 0.f) ? 0.f : v;
+      }
+      comp[r] = (static_cast<uint64_t>(dist_key(v, IS_IP)) << 32) | static_cast<uint32_t>(r);
+    }
+  }
+}
+
+// Selection for the slots fallback_dist_kernel filled: one 1024-thread CTA
+// per failed query (the radix passes over n composites are latency-bound).
+template <bool IS_IP>
+__global__ void __launch_bounds__(1024) fallback_select_kernel(const int* __restrict__ fail_count,
+                                                               const int* __restrict__ fail_list, int nslots, int64_t n,
+                                                               int k, const int64_t* __restrict__ ids,
+                                                               float* __restrict__ D, int64_t* __restrict__ I,
+                                                               int64_t* __restrict__ P, const uint64_t* __restrict__ scratch) {
+  extern __shared__ uint64_t win[];
+  __shared__ int count;
+  __shared__ uint32_t hist[256], sel[8];
+  const int nf = min(*fail_count, nslots);
+  for (int f = blockIdx.x; f < nf; f += gridDim.x)
+    block_select_write<IS_IP>(scratch + (size_t)f * n, (int)n, k, fail_list[f], win, &count, hist, sel, ids, D, I, P);
+}
+
 // Exact fallback, on the device: CTA b takes failed queries b, b+grid, ...;
 // exact composites of every row into its scratch slot, block radix select of
 // the k-th, bitonic sort of the winners.  Launched after every MODE 4 merge
@@ -777,7 +831,8 @@ __global__ void __launch_bounds__(256) fallback_kernel(const int* __restrict__ f
   const int tid = threadIdx.x;
   const int nf = *fail_count;
   uint64_t* comp = scratch + (size_t)blockIdx.x * n;
-  for (int f = blockIdx.x; f < nf; f += gridDim.x) {
+  // failed queries f < grid were answered by fallback_dist/select_kernel
+  for (int f = blockIdx.x + gridDim.x; f < nf; f += gridDim.x) {
     const int q = fail_list[f];
     const float qn = qnorm[q];
     const float4* qh = reinterpret_cast<const float4*>(q0 + (size_t)q * dp);
