@@ -13,7 +13,7 @@ for c in 2 2 1 3 4 5; do
   tail -1 gpurun_out/bench_${TAG}_cfg$c.json | cut -c1-300
 done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_${TAG}.csv \
-   python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/launches_bench_${TAG}.log 2>&1; echo "launches rc=$?"
+   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-gate > gpurun_out/launches_bench_${TAG}.log 2>&1; echo "launches rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:fused_knn -s 2 -c 1 \
    -o gpurun_out/full2_${TAG} -f python scripts/prof_search.py --config 2 --iters 3 > gpurun_out/ncu_full2_${TAG}.log 2>&1; echo "ncu cfg2 rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:fused_knn -s 2 -c 1 \
