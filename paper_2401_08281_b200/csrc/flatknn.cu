@@ -1045,9 +1045,11 @@ int search_mode4(fk_index* h, int64_t nq, int k, bool ip, float* dD, int64_t* dI
   // over every SM: S_tot k' entries per query) gets room for all of its list
   // and overflow entries -- few CTAs, and an overflow would send the query to
   // the exact fallback (a scan of the whole base per query)
+  // (any batch size: when every list entry could survive -- e.g. 32-deep
+  // queues over many lists -- an overflow would send the query to the exact
+  // fallback; a larger buffer only costs merge occupancy)
   int smc = std::min(MERGE_SMC, std::max(1024, 24 * kp));
-  if (nq <= 4 * (int64_t)h->num_sms)
-    smc = std::min(MERGE_SMC, std::max<int>(smc, pl.S_tot * kp + ovf_cap));
+  smc = std::min(MERGE_SMC, std::max<int>(smc, pl.S_tot * kp + ovf_cap));
   int p2 = 1;
   while (p2 < k) p2 <<= 1;
   static std::atomic<uint64_t> cfg{0};

@@ -231,14 +231,16 @@ def test_filter16_coherent_rounding_worst_case(filt):
     assert_parity(res.ids, res.distances, want_ids, want_dist)
 
 
-def test_filter16_fallback_values_equal_certified_values():
+@pytest.mark.parametrize("nq", [200, 600])
+def test_filter16_fallback_values_equal_certified_values(nq):
     """Queries forced into the exact fallback (no overflow lists, 8-deep
     queues) return bit-identical values and ids to the certified rescoring
     merge: both sum the fp32 products in the same order (warp_exact_dot /
-    thread_exact_dot)."""
+    thread_exact_dot).  600 queries: past the first 148 failed queries (rows
+    split over the grid) the per-CTA whole-base scan answers the rest."""
     rng = np.random.default_rng(21)
     xb = rng.standard_normal((70000, 96), dtype=np.float32)
-    q = rng.standard_normal((200, 96), dtype=np.float32)
+    q = rng.standard_normal((nq, 96), dtype=np.float32)
     idx = _index(96, "l2")
     idx.add(xb)
     base = idx.search(q, 10)
