@@ -564,7 +564,7 @@ __global__ void __launch_bounds__(256) merge_rescore_kernel(
 // warp-private smem buffer (W_SMW entries; more -> exact fallback), ranks by
 // counting instead of block-wide radix selects, the same certification, band
 // and warp_exact_dot rescoring (values bit-identical to the CTA form).
-constexpr int W_SMW = 256;
+constexpr int W_SMW = 512;
 template <bool IS_IP>
 __global__ void __launch_bounds__(256) merge_rescore_warp_kernel(
     const uint32_t* __restrict__ pkey, const uint32_t* __restrict__ ppos, int S, int nq, int kp, int k,
